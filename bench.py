@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""bench.py — edges coloured per second (GTEPS) of the B200 SGR colouring path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat24] [--impl ours|reference]
+
+A "step" is one whole gc_color call (ingest + every SGR round + finalize) on the
+BASELINE.json workload, inputs resident in HBM.  Prints ONE JSON line (rank 0).
+See DESIGN.md §7 for the roofline bytes, the CPU baseline sample and the e2e leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edges colored/sec (GTEPS)"
+UNIT = "GTEPS"
+
+# bounded CPU-oracle samples of each workload family (~10-30 s of single-core CPU work)
+CPU_SAMPLES = {
+    "rmat24": ("rmat", dict(scale=21, edge_factor=16)),
+    "rmat16": ("rmat", dict(scale=16, edge_factor=8)),
+    "stencil128": ("stencil", dict(nx=96)),
+    "mesh8192": ("mesh", dict(rows=4096, cols=4096, p_delete=0.3)),
+    "rmat27": ("rmat", dict(scale=21, edge_factor=16)),
+}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def sample_graph(cfg):
+    import workloads as wl
+    kind, kw = CPU_SAMPLES[cfg]
+    if kind == "rmat":
+        return wl.rmat(kw["scale"], kw["edge_factor"]), f"R-MAT scale {kw['scale']} ef {kw['edge_factor']} (same generator/params as {cfg})"
+    if kind == "stencil":
+        return wl.stencil27(kw["nx"]), f"27-point stencil {kw['nx']}^3 (same generator as {cfg})"
+    return wl.mesh2d(kw["rows"], kw["cols"], kw["p_delete"]), f"mesh {kw['rows']}x{kw['cols']} 30% deleted (same generator as {cfg})"
+
+
+def cpu_oracle_gteps(cfg):
+    """Time the CPU oracle as it stands (single-threaded C) on a bounded sample."""
+    import oracle
+    g, desc = sample_graph(cfg)
+    t0 = time.perf_counter()
+    _, nc, r = oracle.sgr(g)
+    dt = time.perf_counter() - t0
+    return dict(value=g.m / dt / 1e9, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{desc}: n={g.n} m={g.m}, full oracle_sgr run, {dt:.2f} s, {r} rounds, {nc} colors",
+                seconds=dt)
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for k, bit in names.items():
+                        if r & bit and k != "gpu_idle":
+                            self.reasons.add(k)
+                except Exception:
+                    pass
+                time.sleep(0.005)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def algorithmic_bytes(work, n):
+    """Bytes the implemented algorithm must move per launch (DESIGN.md §7 per-unit table)."""
+    return (44 * n                                   # ingest: row_ptr x2, st, fm, W_1
+            + 12 * work["phase_a_vertices"]          # W id, fm read, st write
+            + 8 * work["phase_a_edges"]              # fallback First-Fit: col + st gather
+            + 28 * work["phase_b_vertices"]          # W id, row_ptr pair, own st, commit/push
+            + 4 * work["phase_b_edges"]              # col_idx entries scanned
+            + 4 * work["phase_b_gathers"]            # neighbour colour gathers
+            + 8 * work["commit_scatter"]             # col + forbidden-mask RED
+            + 8 * n)                                 # finalize: st read, colours write
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(cfg):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(cfg)
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle  # noqa: F401  (the reference arm is the CPU oracle)
+    g, desc = sample_graph(args.config)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are not repeated for the CPU arm
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sgr(g)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = g.m / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.config, "sample": desc, "n": g.n, "m": g.m, "policy": "higher_id"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{desc}: n={g.n} m={g.m}, oracle_sgr single-threaded C, mean of {args.steps}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1606_06025_b200 as gc
+    import workloads as wl
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g = wl.config_graph(args.config)
+    n, m = g.n, g.m
+    rp = torch.from_numpy(g.row_ptr).cuda()
+    ci = torch.from_numpy(g.col_idx).cuda()
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    kw = dict(policy=args.policy, validate=False, out=out)
+
+    # untimed instrumented run: exact work counters -> algorithmic bytes per launch
+    wres = gc.color(rp, ci, count_work=True, trace=True, **kw)
+    work = wres.work
+    alg_bytes = algorithmic_bytes(work, n)
+    verified = gc.verify(rp, ci, out) == -1
+
+    for _ in range(args.warmup):
+        gc.color(rp, ci, **kw)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local).start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    kms = []
+    for _ in range(args.steps):
+        r = gc.color(rp, ci, time_kernel=True, **kw)
+        kms.append(r.kernel_ms)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kernel_ms = sum(kms) / len(kms)
+    value = world * m / (ms / 1e3) / 1e9
+
+    # e2e: the same call with pinned HOST buffers (H2D of the CSR and D2H of the colours
+    # inside the timed region, done by the library)
+    e2e = None
+    if not args.no_e2e:
+        h_rp = torch.from_numpy(g.row_ptr).pin_memory()
+        h_ci = torch.from_numpy(g.col_idx).pin_memory()
+        h_out = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
+        h_rp_np, h_ci_np, h_out_np = h_rp.numpy(), h_ci.numpy(), h_out.numpy().view(np.uint32)
+        e2e_steps = max(1, min(args.steps, 10))
+        gc.color(h_rp_np, h_ci_np, policy=args.policy, validate=False, out=h_out_np)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            gc.color(h_rp_np, h_ci_np, policy=args.policy, validate=False, out=h_out_np)
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
+        assert np.array_equal(h_out_np[:n], out.cpu().numpy().view(np.uint32)[:n])
+        e2e = {"value": m / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * (n + 1) + 4 * m, "d2h_bytes_per_step": 4 * n + 224}
+
+    peaks, src = measured_peaks()
+    peak = float(peaks["hbm_gbs"])
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.config)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_gteps(args.config)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": args.config, "n": n, "m": m, "policy": args.policy,
+                       "validate": False, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB); no flush" % ((8 * (n + 1) + 4 * m) / 1e9)},
+            "num_colors": wres.num_colors, "rounds": wres.rounds, "verified_ff_fixpoint": verified,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{src} hbm_gbs", "kernel": "sgr_persistent",
+                         "kernel_ms": kernel_ms, "alg_bytes_per_launch": alg_bytes},
+            "work": work,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="rmat24")
+    ap.add_argument("--policy", default="higher_id")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

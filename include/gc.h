@@ -1,0 +1,153 @@
+/*
+ * gc.h — C ABI of the B200-native round-synchronous speculative-greedy (SGR) graph
+ * colouring library (arXiv 1606.06025).  Library: paper_1606_06025_b200/libgc.so.
+ *
+ * The library colours an undirected graph given in CSR form (§3 "The
+ * column-indices array C ... The row-offsets R array contains n + 1 integers") with the
+ * data-driven speculative greedy loop of Alg. 7 "Data-driven Parallel Graph Coloring"
+ * = Alg. 2 GM with FirstFit (Alg. 4,
+ * PAPER.md:327-338) and ConflictResolve (Alg. 5), made round-synchronous
+ * (Jacobi) as the north star requires: every round, Phase A reads the colours committed
+ * before the round, Phase B reads the round's tentative colours.  The result is therefore
+ * a pure function of the graph and the policy, identical to the CPU oracle (oracle/),
+ * independent of thread schedule, launch geometry and (for gc_color_dist) partitioning.
+ *
+ * Conventions common to every entry point:
+ *  - The caller owns every buffer.  The library keeps no pointer after return.
+ *  - Pointers may be host memory or device memory of the selected device; the space is
+ *    detected with cudaPointerGetAttributes.  Host inputs are copied to the device and
+ *    host outputs copied back inside the call.
+ *  - Calls are synchronous: they return after every output is final (one stream sync).
+ *  - On error every scalar output is set to 0, array outputs are unspecified, nothing is
+ *    thrown or aborted, and a human-readable detail is available from
+ *    gc_last_error_message() (thread-local).
+ *  - No global mutable state other than a per-device workspace memory pool; concurrent
+ *    calls on distinct streams are allowed.
+ */
+#ifndef GC_H_
+#define GC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+typedef enum gc_status {
+  GC_OK = 0,
+  GC_ERR_INVALID_ARGUMENT = 1, /* NULL with n>0, n<0, n>INT32_MAX, bad struct_size/policy */
+  GC_ERR_INVALID_GRAPH = 2,    /* row_ptr[0]!=0 / decreasing, col out of range, self loop,
+                                  unsorted or duplicate row entry, asymmetric edge
+                                  (only detected when the matching GC_FLAG_VALIDATE* is set) */
+  GC_ERR_NO_CONVERGENCE = 3,   /* rounds would exceed max_rounds */
+  GC_ERR_OUT_OF_MEMORY = 4,
+  GC_ERR_CUDA = 5,             /* CUDA runtime error or device-side watchdog; see message */
+  GC_ERR_NCCL = 6,
+  GC_ERR_UNSUPPORTED = 7       /* no sm_100-class device, no cooperative launch, ... */
+} gc_status;
+
+/* Which endpoint of a same-colour edge {v, w} is re-queued (recolours). */
+typedef enum gc_policy {
+  GC_POLICY_HIGHER_ID = 0, /* default: the higher vertex id recolours (BASELINE north star) */
+  GC_POLICY_LOWER_ID = 1,  /* Alg. 5 literal "color[v]=color[w] and v<w" clears v */
+  GC_POLICY_DEGREE = 2     /* §3.2 heuristic: smaller static degree
+                              recolours; equal degree -> the smaller id is picked (keeps it) */
+} gc_policy;
+
+enum {
+  GC_FLAG_VALIDATE = 1u,          /* check CSR invariants S:22-32 (one pass over col_idx) */
+  GC_FLAG_VALIDATE_SYMMETRY = 2u, /* also check w in adj(v) <=> v in adj(w) (O(m log deg)) */
+  GC_FLAG_TRACE = 4u,             /* write |W_r| for r = 1..rounds into opts->trace_worklist */
+  GC_FLAG_PULL_FIRSTFIT = 8u,     /* Phase A by a full neighbour scan each round (the paper's
+                                     FirstFit) instead of the incremental forbidden-colour mask;
+                                     same result, more traffic; ablation */
+  GC_FLAG_HOST_ROUNDS = 16u,      /* one kernel launch per phase with the host reading |W| each
+                                     round (the paper's baseline control) instead of
+                                     the persistent kernel; same result; ablation */
+  GC_FLAG_COUNT_WORK = 32u        /* fill opts->work with exact work counters (slower) */
+};
+
+/* Exact work counters (GC_FLAG_COUNT_WORK); the run is deterministic, so these are a pure
+ * function of (graph, policy, flags).  Used for the algorithmic-byte roofline. */
+typedef struct gc_work {
+  uint64_t phase_a_vertices;   /* sum over rounds r >= 2 of |W_r| (round 1 needs no Phase A) */
+  uint64_t phase_a_edges;      /* neighbour words gathered in Phase A (full scans/fallbacks) */
+  uint64_t phase_b_vertices;   /* sum over rounds of |W_r| */
+  uint64_t phase_b_edges;      /* col_idx entries examined by the conflict scans */
+  uint64_t phase_b_gathers;    /* neighbour colour words gathered by the conflict scans */
+  uint64_t commit_scatter;     /* forbidden-mask atomics issued by committing vertices */
+  uint64_t pushes;             /* vertices pushed into W_out over the run */
+  uint64_t reserved[9];
+} gc_work;
+
+typedef struct gc_opts {
+  uint32_t struct_size;      /* = sizeof(gc_opts) (ABI check) */
+  uint32_t policy;           /* gc_policy */
+  uint32_t flags;            /* GC_FLAG_*; default GC_FLAG_VALIDATE */
+  uint32_t max_rounds;       /* 0 -> n + 1 (reading C13) */
+  int32_t device;            /* CUDA ordinal; -1 = the calling thread's current device */
+  uint32_t thread_bin_max;   /* degree <= this -> one thread per vertex (0 -> default 16) */
+  uint32_t warp_bin_max;     /* degree <= this -> one warp per vertex (0 -> default 4096);
+                                larger degrees -> one CTA per vertex */
+  uint32_t blocks_per_sm;    /* persistent grid = SMs x this (0 -> max co-resident) */
+  void* stream;              /* cudaStream_t to run on; NULL = library-internal stream */
+  uint32_t* trace_worklist;  /* host or device, [trace_capacity]; used with GC_FLAG_TRACE */
+  uint32_t trace_capacity;
+  uint32_t reserved0;
+  gc_work* work;             /* host pointer; used with GC_FLAG_COUNT_WORK */
+  float* kernel_ms;          /* optional host pointer: device time (CUDA events on the call's
+                                stream) from the first to the last colouring kernel, i.e.
+                                excluding argument checks, copies and validation */
+  uint64_t reserved[3];
+} gc_opts;
+
+/* Fill *o with the defaults above (policy HIGHER_ID, flags GC_FLAG_VALIDATE). */
+void gc_opts_default(gc_opts* o);
+
+/*
+ * gc_color — colour the undirected CSR graph (n, row_ptr, col_idx).
+ *   n          number of vertices, 0 <= n <= INT32_MAX.
+ *   row_ptr    int64[n+1], row offsets R; m = row_ptr[n] = directed
+ *              adjacency entries (reading C15).
+ *   col_idx    int32[m], column indices C; each row sorted strictly increasing, no self
+ *              loop, symmetric (checked only under GC_FLAG_VALIDATE*).
+ *   opts       NULL = gc_opts_default.
+ *   colors_out uint32[n]: colour of every vertex, 1..Delta+1 (0 = sentinel never returned).
+ *   num_colors max colour (= number of distinct colours, First-Fit fixpoint).
+ *   rounds     number of SGR rounds (Phase-A passes; PAPER.md:427 loop iterations).
+ * n = 0 returns GC_OK with num_colors = rounds = 0.
+ */
+gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                   const gc_opts* opts, uint32_t* colors_out, uint32_t* num_colors,
+                   uint32_t* rounds);
+
+/*
+ * gc_verify — device check that `colors` is complete (all >= 1), proper (no edge with equal
+ * colours) and a First-Fit fixpoint (every colour is the smallest colour
+ * absent from its neighbourhood, which every SGR result satisfies).
+ *   *bad_vertex = first offending vertex found (any one), or -1 when valid.
+ * Returns GC_OK when valid, GC_ERR_INVALID_GRAPH when a violation was found.
+ */
+gc_status gc_verify(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                    const uint32_t* colors, int32_t device, int64_t* bad_vertex);
+
+const char* gc_status_string(gc_status s);
+const char* gc_last_error_message(void);
+
+/*
+ * gc_partition_edge_balanced — host-only helper for the vertex-range multi-GPU path
+ * (SURVEY §8(e)): bounds[k] = min{v : row_ptr[v] >= ceil(k*m/parts)} for k = 0..parts,
+ * bounds[0] = 0, bounds[parts] = n.  row_ptr must be host memory.
+ */
+gc_status gc_partition_edge_balanced(int64_t n, const int64_t* row_ptr, int32_t parts,
+                                     int64_t* bounds);
+
+/* ABI version of the loaded library (== GC_ABI_VERSION it was built with). */
+int32_t gc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC_H_ */

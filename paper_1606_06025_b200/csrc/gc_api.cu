@@ -1,0 +1,510 @@
+// gc_api.cu — host side of the C ABI declared in include/gc.h.
+// Argument checking, pointer-space detection, workspace from a per-device stream-ordered
+// memory pool, one cooperative launch of the persistent SGR kernel, one stream sync.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/gc.h"
+#include "sgr_kernels.cuh"
+
+using namespace gcdev;
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+constexpr int kMaxDev = 64;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDev] = {};
+
+gc_status cuda_fail(cudaError_t e, const char* what) {
+  set_err("%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? GC_ERR_OUT_OF_MEMORY : GC_ERR_CUDA;
+}
+
+#define CK(call)                                      \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+cudaError_t get_pool(int dev, cudaMemPool_t* out) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;  // keep freed blocks cached across calls
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pool[dev] = pool;
+  }
+  *out = g_pool[dev];
+  return cudaSuccess;
+}
+
+// Restores the caller's current device; frees pool allocations stream-ordered; owns an
+// internal stream when the caller passed none.
+struct Scope {
+  int prev_dev = -1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaMemPool_t pool = nullptr;
+  void* ptrs[16];
+  int nptr = 0;
+  ~Scope() {
+    for (int i = 0; i < nptr; ++i) cudaFreeAsync(ptrs[i], stream);
+    if (stream) cudaStreamSynchronize(stream);
+    if (own_stream) cudaStreamDestroy(stream);
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);
+  }
+  cudaError_t alloc(void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocFromPoolAsync(p, bytes, pool, stream);
+    if (e == cudaSuccess) ptrs[nptr++] = *p;
+    return e;
+  }
+};
+
+// 1 = device (or managed) memory usable by kernels, 0 = host memory, -1 = error
+int is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
+}
+
+using PersistentFn = void (*)(Params);
+
+template <int POL, bool PUSH, bool CW>
+void* persistent_ptr() { return (void*)sgr_persistent<POL, PUSH, CW>; }
+
+void* pick_persistent(int pol, bool push, bool cw) {
+#define PK(P)                                                                             \
+  if (pol == P) {                                                                         \
+    if (push) return cw ? persistent_ptr<P, true, true>() : persistent_ptr<P, true, false>(); \
+    return cw ? persistent_ptr<P, false, true>() : persistent_ptr<P, false, false>();     \
+  }
+  PK(HIGHER_ID) PK(LOWER_ID) PK(DEGREE)
+#undef PK
+  return nullptr;
+}
+
+template <int POL, bool PUSH, bool CW>
+void launch_phase_b(int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W, int32_t* Wo) {
+  k_phase_b<POL, PUSH, CW><<<grid, BLOCK, 0, s>>>(p, r, W, Wo);
+}
+template <bool PUSH, bool CW>
+void launch_phase_a(int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W) {
+  k_phase_a<PUSH, CW><<<grid, BLOCK, 0, s>>>(p, r, W);
+}
+
+void launch_b(int pol, bool push, bool cw, int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W, int32_t* Wo) {
+#define LB(P)                                                                   \
+  if (pol == P) {                                                               \
+    if (push) { if (cw) launch_phase_b<P, true, true>(grid, s, p, r, W, Wo); else launch_phase_b<P, true, false>(grid, s, p, r, W, Wo); } \
+    else { if (cw) launch_phase_b<P, false, true>(grid, s, p, r, W, Wo); else launch_phase_b<P, false, false>(grid, s, p, r, W, Wo); } \
+    return;                                                                     \
+  }
+  LB(HIGHER_ID) LB(LOWER_ID) LB(DEGREE)
+#undef LB
+}
+
+const char* val_err_name(uint32_t code) {
+  switch (code) {
+    case VE_ROWPTR: return "row_ptr[0] != 0 or row_ptr decreasing";
+    case VE_RANGE: return "col_idx entry out of range [0, n)";
+    case VE_SELF: return "self loop";
+    case VE_ORDER: return "row not strictly increasing (unsorted or duplicate entry)";
+    case VE_ASYM: return "asymmetric edge (w in adj(v) but v not in adj(w))";
+    default: return "invalid graph";
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t gc_abi_version(void) { return GC_ABI_VERSION; }
+
+void gc_opts_default(gc_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(gc_opts);
+  o->policy = GC_POLICY_HIGHER_ID;
+  o->flags = GC_FLAG_VALIDATE;
+  o->max_rounds = 0;
+  o->device = -1;
+}
+
+const char* gc_status_string(gc_status s) {
+  switch (s) {
+    case GC_OK: return "GC_OK";
+    case GC_ERR_INVALID_ARGUMENT: return "GC_ERR_INVALID_ARGUMENT";
+    case GC_ERR_INVALID_GRAPH: return "GC_ERR_INVALID_GRAPH";
+    case GC_ERR_NO_CONVERGENCE: return "GC_ERR_NO_CONVERGENCE";
+    case GC_ERR_OUT_OF_MEMORY: return "GC_ERR_OUT_OF_MEMORY";
+    case GC_ERR_CUDA: return "GC_ERR_CUDA";
+    case GC_ERR_NCCL: return "GC_ERR_NCCL";
+    case GC_ERR_UNSUPPORTED: return "GC_ERR_UNSUPPORTED";
+  }
+  return "GC_ERR_UNKNOWN";
+}
+
+const char* gc_last_error_message(void) { return g_err; }
+
+gc_status gc_partition_edge_balanced(int64_t n, const int64_t* row_ptr, int32_t parts, int64_t* bounds) {
+  if (n < 0 || parts < 1 || !bounds || (n > 0 && !row_ptr)) {
+    set_err("gc_partition_edge_balanced: invalid argument");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  const int64_t m = n > 0 ? row_ptr[n] : 0;
+  bounds[0] = 0;
+  for (int32_t k = 1; k < parts; ++k) {
+    // target = ceil(k*m/parts) without overflow for m < 2^62
+    const __int128 num = (__int128)k * m;
+    const int64_t target = (int64_t)((num + parts - 1) / parts);
+    int64_t lo = 0, hi = n;  // smallest v with row_ptr[v] >= target
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (row_ptr[mid] >= target) hi = mid; else lo = mid + 1;
+    }
+    bounds[k] = lo < bounds[k - 1] ? bounds[k - 1] : lo;
+  }
+  bounds[parts] = n;
+  return GC_OK;
+}
+
+gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const gc_opts* opts_in,
+                   uint32_t* colors_out, uint32_t* num_colors, uint32_t* rounds) {
+  g_err[0] = 0;
+  if (!num_colors || !rounds) {
+    set_err("gc_color: num_colors and rounds must not be NULL");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  *num_colors = 0;
+  *rounds = 0;
+  gc_opts o;
+  gc_opts_default(&o);
+  if (opts_in) {
+    if (opts_in->struct_size != sizeof(gc_opts)) {
+      set_err("gc_color: opts->struct_size=%u, expected %zu", opts_in->struct_size, sizeof(gc_opts));
+      return GC_ERR_INVALID_ARGUMENT;
+    }
+    o = *opts_in;
+  }
+  if (o.policy > GC_POLICY_DEGREE) {
+    set_err("gc_color: unknown policy %u", o.policy);
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  if (n < 0 || n > INT32_MAX) {
+    set_err("gc_color: n=%lld out of range [0, 2^31-1]", (long long)n);
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return GC_OK;
+  if (!row_ptr || !col_idx || !colors_out) {
+    set_err("gc_color: NULL row_ptr/col_idx/colors_out with n=%lld", (long long)n);
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  if ((o.flags & GC_FLAG_TRACE) && o.trace_capacity && !o.trace_worklist) {
+    set_err("gc_color: GC_FLAG_TRACE with NULL trace_worklist");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  if ((o.flags & GC_FLAG_COUNT_WORK) && !o.work) {
+    set_err("gc_color: GC_FLAG_COUNT_WORK with NULL work");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+
+  Scope sc;
+  CK(cudaGetDevice(&sc.prev_dev));
+  const int dev = o.device >= 0 ? o.device : sc.prev_dev;
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) {
+    set_err("gc_color: device %d is sm_%d%d; this library is built for sm_100a", dev, prop.major, prop.minor);
+    return GC_ERR_UNSUPPORTED;
+  }
+  if (o.stream) {
+    sc.stream = (cudaStream_t)o.stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+    sc.own_stream = true;
+  }
+  CK(get_pool(dev, &sc.pool));
+  cudaStream_t s = sc.stream;
+
+  // ---- inputs in device memory
+  const bool rp_dev = is_device_ptr(row_ptr) == 1;
+  const bool ci_dev = is_device_ptr(col_idx) == 1;
+  const bool out_dev = is_device_ptr(colors_out) == 1;
+  const int64_t* d_rp = row_ptr;
+  const int32_t* d_ci = col_idx;
+  int64_t m = -1;
+  if (!rp_dev) {
+    m = row_ptr[n];
+    void* p;
+    CK(sc.alloc(&p, sizeof(int64_t) * (size_t)(n + 1)));
+    CK(cudaMemcpyAsync(p, row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
+    d_rp = (const int64_t*)p;
+  }
+  if (!ci_dev) {
+    if (m < 0) {
+      CK(cudaMemcpyAsync(&m, d_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    if (m < 0) {
+      set_err("gc_color: row_ptr[n]=%lld < 0", (long long)m);
+      return GC_ERR_INVALID_GRAPH;
+    }
+    void* p;
+    CK(sc.alloc(&p, sizeof(int32_t) * (size_t)m));
+    if (m) CK(cudaMemcpyAsync(p, col_idx, sizeof(int32_t) * (size_t)m, cudaMemcpyHostToDevice, s));
+    d_ci = (const int32_t*)p;
+  }
+
+  // ---- workspace
+  const bool push = !(o.flags & GC_FLAG_PULL_FIRSTFIT);
+  const bool cw = (o.flags & GC_FLAG_COUNT_WORK) != 0;
+  void *st, *fm = nullptr, *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
+  CK(sc.alloc(&st, sizeof(uint32_t) * (size_t)n));
+  if (push) CK(sc.alloc(&fm, sizeof(uint32_t) * (size_t)n));
+  CK(sc.alloc(&w0, sizeof(int32_t) * (size_t)n));
+  CK(sc.alloc(&w1, sizeof(int32_t) * (size_t)n));
+  CK(sc.alloc(&info, sizeof(DevInfo)));
+  CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
+  if (!out_dev) CK(sc.alloc(&dcol, sizeof(uint32_t) * (size_t)n));
+  const bool trace = (o.flags & GC_FLAG_TRACE) && o.trace_capacity;
+  const bool trace_dev = trace && is_device_ptr(o.trace_worklist) == 1;
+  if (trace) {
+    if (trace_dev) dtrace = o.trace_worklist;
+    else CK(sc.alloc(&dtrace, sizeof(uint32_t) * o.trace_capacity));
+  }
+
+  // ---- optional validation (C9): one warp per vertex
+  if (o.flags & (GC_FLAG_VALIDATE | GC_FLAG_VALIDATE_SYMMETRY)) {
+    const int vgrid = prop.multiProcessorCount * 8;
+    k_validate<<<vgrid, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, (o.flags & GC_FLAG_VALIDATE_SYMMETRY) ? 1 : 0,
+                                       (DevInfo*)info);
+    CK(cudaGetLastError());
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&bad, &((DevInfo*)info)->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad) {
+      bad -= 1;
+      set_err("gc_color: invalid graph at vertex %llu: %s", bad >> 3, val_err_name((uint32_t)(bad & 7)));
+      return GC_ERR_INVALID_GRAPH;
+    }
+  }
+
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.n = (int32_t)n;
+  p.rp = d_rp;
+  p.ci = d_ci;
+  p.st = (uint32_t*)st;
+  p.fm = (uint32_t*)fm;
+  p.wl0 = (int32_t*)w0;
+  p.wl1 = (int32_t*)w1;
+  p.info = (DevInfo*)info;
+  p.trace = (uint32_t*)dtrace;
+  p.trace_cap = trace ? o.trace_capacity : 0;
+  p.colors_out = (uint32_t*)dcol;
+  p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
+  p.tb = o.thread_bin_max ? o.thread_bin_max : 16;
+  p.wb = o.warp_bin_max ? o.warp_bin_max : 4096;
+  if (p.wb < p.tb) p.wb = p.tb;
+  p.timeout_ns = 60ull * 1000000000ull;
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (o.kernel_ms) {
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, s));
+  }
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+  } evg{ev0, ev1};
+  if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
+    // ---- persistent cooperative kernel: the whole run in one launch
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) {
+      set_err("gc_color: device %d does not support cooperative launch", dev);
+      return GC_ERR_UNSUPPORTED;
+    }
+    void* fn = pick_persistent((int)o.policy, push, cw);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0));
+    if (per_sm < 1) {
+      set_err("gc_color: persistent kernel cannot be resident");
+      return GC_ERR_UNSUPPORTED;
+    }
+    if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
+    const int grid = prop.multiProcessorCount * per_sm;
+    void* args[] = {&p};
+    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s));
+  } else {
+    // ---- host-driven rounds (ablation): one launch per phase, |W| read every round
+    const int grid = prop.multiProcessorCount * 4;
+    if (push) k_prologue_count<true><<<grid, BLOCK, 0, s>>>(p);
+    else k_prologue_count<false><<<grid, BLOCK, 0, s>>>(p);
+    k_prologue_scatter<<<grid, BLOCK, 0, s>>>(p);
+    CK(cudaGetLastError());
+    int32_t* W = p.wl0;
+    int32_t* Wo = p.wl1;
+    uint32_t r = 1;
+    uint32_t cnt[3][NBIN];
+    for (;;) {
+      if (r > 1) {
+        if (push) { if (cw) launch_phase_a<true, true>(grid, s, p, r, W); else launch_phase_a<true, false>(grid, s, p, r, W); }
+        else { if (cw) launch_phase_a<false, true>(grid, s, p, r, W); else launch_phase_a<false, false>(grid, s, p, r, W); }
+      }
+      launch_b((int)o.policy, push, cw, grid, s, p, r, W, Wo);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(cnt, ((DevInfo*)info)->cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const uint32_t* nx = cnt[(r + 1) % 3];
+      if (nx[0] + nx[1] + nx[2] == 0) break;
+      if (r >= p.max_rounds) {
+        set_err("gc_color: no convergence within max_rounds=%u", p.max_rounds);
+        return GC_ERR_NO_CONVERGENCE;
+      }
+      ++r;
+      int32_t* t = W;
+      W = Wo;
+      Wo = t;
+    }
+    k_epilogue<<<grid, BLOCK, 0, s>>>(p, r);
+  }
+  CK(cudaGetLastError());
+  if (ev1) CK(cudaEventRecord(ev1, s));
+
+  DevInfo hinfo;
+  CK(cudaMemcpyAsync(&hinfo, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+  if (!out_dev) CK(cudaMemcpyAsync(colors_out, dcol, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ev1) CK(cudaEventElapsedTime(o.kernel_ms, ev0, ev1));
+  if (hinfo.status == ST_WATCHDOG) {
+    set_err("gc_color: device watchdog fired (grid barrier timeout)");
+    return GC_ERR_CUDA;
+  }
+  if (hinfo.status == ST_NO_CONVERGENCE) {
+    set_err("gc_color: no convergence within max_rounds=%u", p.max_rounds);
+    return GC_ERR_NO_CONVERGENCE;
+  }
+  if (trace && !trace_dev) {
+    const uint32_t k = hinfo.rounds < o.trace_capacity ? hinfo.rounds : o.trace_capacity;
+    if (k) {
+      CK(cudaMemcpyAsync(o.trace_worklist, dtrace, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  if (cw) {
+    memset(o.work, 0, sizeof(gc_work));
+    o.work->phase_a_vertices = hinfo.work[W_A_VERT];
+    o.work->phase_a_edges = hinfo.work[W_A_EDGE];
+    o.work->phase_b_vertices = hinfo.work[W_B_VERT];
+    o.work->phase_b_edges = hinfo.work[W_B_EDGE];
+    o.work->phase_b_gathers = hinfo.work[W_B_GATHER];
+    o.work->commit_scatter = hinfo.work[W_SCATTER];
+    o.work->pushes = hinfo.work[W_PUSH];
+  }
+  *num_colors = hinfo.num_colors;
+  *rounds = hinfo.rounds;
+  return GC_OK;
+}
+
+gc_status gc_verify(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const uint32_t* colors,
+                    int32_t device, int64_t* bad_vertex) {
+  g_err[0] = 0;
+  if (!bad_vertex) {
+    set_err("gc_verify: bad_vertex must not be NULL");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  *bad_vertex = -1;
+  if (n < 0 || n > INT32_MAX) {
+    set_err("gc_verify: n out of range");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return GC_OK;
+  if (!row_ptr || !col_idx || !colors) {
+    set_err("gc_verify: NULL pointer");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  Scope sc;
+  CK(cudaGetDevice(&sc.prev_dev));
+  const int dev = device >= 0 ? device : sc.prev_dev;
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+  sc.own_stream = true;
+  CK(get_pool(dev, &sc.pool));
+  cudaStream_t s = sc.stream;
+  const int64_t* d_rp = row_ptr;
+  const int32_t* d_ci = col_idx;
+  const uint32_t* d_col = colors;
+  int64_t m = -1;
+  if (is_device_ptr(row_ptr) != 1) {
+    m = row_ptr[n];
+    void* p;
+    CK(sc.alloc(&p, sizeof(int64_t) * (size_t)(n + 1)));
+    CK(cudaMemcpyAsync(p, row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
+    d_rp = (const int64_t*)p;
+  }
+  if (is_device_ptr(col_idx) != 1) {
+    if (m < 0) {
+      CK(cudaMemcpyAsync(&m, d_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    void* p;
+    CK(sc.alloc(&p, sizeof(int32_t) * (size_t)m));
+    if (m) CK(cudaMemcpyAsync(p, col_idx, sizeof(int32_t) * (size_t)m, cudaMemcpyHostToDevice, s));
+    d_ci = (const int32_t*)p;
+  }
+  if (is_device_ptr(colors) != 1) {
+    void* p;
+    CK(sc.alloc(&p, sizeof(uint32_t) * (size_t)n));
+    CK(cudaMemcpyAsync(p, colors, sizeof(uint32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
+    d_col = (const uint32_t*)p;
+  }
+  void* info;
+  CK(sc.alloc(&info, sizeof(DevInfo)));
+  CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  k_verify<<<prop.multiProcessorCount * 8, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, d_col, (DevInfo*)info);
+  CK(cudaGetLastError());
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, &((DevInfo*)info)->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) {
+    *bad_vertex = (int64_t)((bad - 1) >> 3);
+    set_err("gc_verify: vertex %lld violates %s", (long long)*bad_vertex,
+            ((bad - 1) & 7) == 1 ? "completeness/greedy bound" : "properness/First-Fit fixpoint");
+    return GC_ERR_INVALID_GRAPH;
+  }
+  return GC_OK;
+}
+
+}  // extern "C"
