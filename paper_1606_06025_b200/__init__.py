@@ -54,7 +54,7 @@ class Opts(ctypes.Structure):
                 ("device", ctypes.c_int32), ("thread_bin_max", ctypes.c_uint32),
                 ("warp_bin_max", ctypes.c_uint32), ("blocks_per_sm", ctypes.c_uint32),
                 ("stream", ctypes.c_void_p), ("trace_worklist", ctypes.c_void_p),
-                ("trace_capacity", ctypes.c_uint32), ("reserved0", ctypes.c_uint32),
+                ("trace_capacity", ctypes.c_uint32), ("group_bin_max", ctypes.c_uint32),
                 ("work", ctypes.POINTER(Work)), ("kernel_ms", ctypes.POINTER(ctypes.c_float)),
                 ("reserved", ctypes.c_uint64 * 3)]
 
@@ -115,7 +115,7 @@ def default_opts() -> Opts:
 def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
           symmetry: bool = False, pull_firstfit: bool = False, host_rounds: bool = False,
           trace: bool = False, count_work: bool = False, max_rounds: int = 0,
-          thread_bin_max: int = 0, warp_bin_max: int = 0, blocks_per_sm: int = 0,
+          thread_bin_max: int = 0, group_bin_max: int = 0, warp_bin_max: int = 0, blocks_per_sm: int = 0,
           stream=None, device: int | None = None, out=None, time_kernel: bool = False) -> ColorResult:
     """gc_color(n, row_ptr, col_idx, opts, colors_out, &num_colors, &rounds) (include/gc.h).
 
@@ -133,6 +133,7 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
     o.max_rounds = max_rounds
     o.thread_bin_max = thread_bin_max
     o.warp_bin_max = warp_bin_max
+    o.group_bin_max = group_bin_max
     o.blocks_per_sm = blocks_per_sm
     dev_inputs = _is_cuda(row_ptr)
     if dev_inputs:
@@ -193,6 +194,19 @@ def partition_edge_balanced(row_ptr, parts: int):
     if st != 0:
         _err(st)
     return bounds
+
+
+_lib.gc__bench_grid_sync.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_float)]
+_lib.gc__bench_grid_sync.restype = ctypes.c_int
+
+
+def bench_grid_sync(device: int = 0, blocks_per_sm: int = 0, iters: int = 2000) -> float:
+    """Diagnostics: microseconds per grid barrier of the persistent kernel."""
+    us = ctypes.c_float()
+    st = _lib.gc__bench_grid_sync(device, blocks_per_sm, iters, ctypes.byref(us))
+    if st != 0:
+        _err(st)
+    return float(us.value)
 
 
 def status_string(s: int) -> str:

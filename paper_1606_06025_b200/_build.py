@@ -44,7 +44,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 def load() -> ctypes.CDLL:
     """Load libgc.so (building it if stale).  Raises if it cannot be built or loaded:
-    the product path has no CPU fallback."""
+    the product path has no CPU fallback.  GC_LIB_PATH overrides the path (debug builds)."""
+    if os.environ.get("GC_LIB_PATH"):
+        return ctypes.CDLL(os.environ["GC_LIB_PATH"])
     try:
         path = build()
     except (OSError, subprocess.CalledProcessError) as e:  # pragma: no cover

@@ -6,10 +6,12 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <mutex>
 
 #include "../../include/gc.h"
+#include "../../include/gc_internal.h"
 #include "sgr_kernels.cuh"
 
 using namespace gcdev;
@@ -60,6 +62,43 @@ cudaError_t get_pool(int dev, cudaMemPool_t* out) {
   return cudaSuccess;
 }
 
+// Per-device facts queried once (cudaGetDeviceProperties costs ~ms; attributes are cheap).
+struct DevFacts {
+  bool ready = false;
+  int sms = 0, major = 0, minor = 0, coop = 0;
+};
+DevFacts g_facts[kMaxDev];
+
+cudaError_t dev_facts(int dev, DevFacts* f) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  DevFacts& d = g_facts[dev];
+  if (!d.ready) {
+    cudaError_t e;
+    if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&d.coop, cudaDevAttrCooperativeLaunch, dev)) != cudaSuccess) return e;
+    d.ready = true;
+  }
+  *f = d;
+  return cudaSuccess;
+}
+
+// Max co-resident CTAs per SM of a kernel, cached per (device, kernel).
+struct OccEntry { int dev; const void* fn; int per_sm; };
+OccEntry g_occ[256];
+int g_nocc = 0;
+
+cudaError_t occupancy(int dev, const void* fn, int* per_sm) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (int i = 0; i < g_nocc; ++i)
+    if (g_occ[i].dev == dev && g_occ[i].fn == fn) { *per_sm = g_occ[i].per_sm; return cudaSuccess; }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, BLOCK, 0);
+  if (e == cudaSuccess && g_nocc < 256) g_occ[g_nocc++] = OccEntry{dev, fn, *per_sm};
+  return e;
+}
+
 // Restores the caller's current device; frees pool allocations stream-ordered; owns an
 // internal stream when the caller passed none.
 struct Scope {
@@ -77,7 +116,11 @@ struct Scope {
   }
   cudaError_t alloc(void** p, size_t bytes) {
     if (bytes == 0) bytes = 16;
+#ifdef GC_DEFAULT_POOL
+    cudaError_t e = cudaMallocAsync(p, bytes, stream);
+#else
     cudaError_t e = cudaMallocFromPoolAsync(p, bytes, pool, stream);
+#endif
     if (e == cudaSuccess) ptrs[nptr++] = *p;
     return e;
   }
@@ -94,20 +137,23 @@ int is_device_ptr(const void* p) {
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
 }
 
-using PersistentFn = void (*)(Params);
+template <class S, int POL, bool PUSH, bool CW>
+void* persistent_ptr() { return (void*)sgr_persistent<S, POL, PUSH, CW>; }
 
-template <int POL, bool PUSH, bool CW>
-void* persistent_ptr() { return (void*)sgr_persistent<POL, PUSH, CW>; }
-
-void* pick_persistent(int pol, bool push, bool cw) {
-#define PK(P)                                                                             \
-  if (pol == P) {                                                                         \
-    if (push) return cw ? persistent_ptr<P, true, true>() : persistent_ptr<P, true, false>(); \
-    return cw ? persistent_ptr<P, false, true>() : persistent_ptr<P, false, false>();     \
+template <class S>
+void* pick_persistent_s(int pol, bool push, bool cw) {
+#define PK(P)                                                                                   \
+  if (pol == P) {                                                                               \
+    if (push) return cw ? persistent_ptr<S, P, true, true>() : persistent_ptr<S, P, true, false>(); \
+    return cw ? persistent_ptr<S, P, false, true>() : persistent_ptr<S, P, false, false>();     \
   }
   PK(HIGHER_ID) PK(LOWER_ID) PK(DEGREE)
 #undef PK
   return nullptr;
+}
+
+void* pick_persistent(bool narrow, int pol, bool push, bool cw) {
+  return narrow ? pick_persistent_s<uint16_t>(pol, push, cw) : pick_persistent_s<uint32_t>(pol, push, cw);
 }
 
 template <int POL, bool PUSH, bool CW>
@@ -239,9 +285,9 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   CK(cudaGetDevice(&sc.prev_dev));
   const int dev = o.device >= 0 ? o.device : sc.prev_dev;
   CK(cudaSetDevice(dev));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, dev));
-  if (prop.major < 10) {
+  DevFacts prop;
+  CK(dev_facts(dev, &prop));
+  if (prop.major != 10) {
     set_err("gc_color: device %d is sm_%d%d; this library is built for sm_100a", dev, prop.major, prop.minor);
     return GC_ERR_UNSUPPORTED;
   }
@@ -303,7 +349,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
 
   // ---- optional validation (C9): one warp per vertex
   if (o.flags & (GC_FLAG_VALIDATE | GC_FLAG_VALIDATE_SYMMETRY)) {
-    const int vgrid = prop.multiProcessorCount * 8;
+    const int vgrid = prop.sms * 8;
     k_validate<<<vgrid, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, (o.flags & GC_FLAG_VALIDATE_SYMMETRY) ? 1 : 0,
                                        (DevInfo*)info);
     CK(cudaGetLastError());
@@ -311,7 +357,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     CK(cudaMemcpyAsync(&bad, &((DevInfo*)info)->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (bad) {
-      bad -= 1;
+      bad = ~bad;
       set_err("gc_color: invalid graph at vertex %llu: %s", bad >> 3, val_err_name((uint32_t)(bad & 7)));
       return GC_ERR_INVALID_GRAPH;
     }
@@ -331,9 +377,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.trace_cap = trace ? o.trace_capacity : 0;
   p.colors_out = (uint32_t*)dcol;
   p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
-  p.tb = o.thread_bin_max ? o.thread_bin_max : 16;
-  p.wb = o.warp_bin_max ? o.warp_bin_max : 4096;
-  if (p.wb < p.tb) p.wb = p.tb;
+  p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
+  p.t2 = o.group_bin_max ? o.group_bin_max : 128;
+  p.t3 = o.warp_bin_max ? o.warp_bin_max : 4096;
+  if (p.t2 < p.t1) p.t2 = p.t1;
+  if (p.t3 < p.t2) p.t3 = p.t2;
   p.timeout_ns = 60ull * 1000000000ull;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -346,28 +394,53 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     cudaEvent_t a, b;
     ~EvGuard() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
   } evg{ev0, ev1};
+  // Optional (diagnostics): L2 set-aside for the evict_last per-vertex state.
+  size_t prev_persist = 0;
+  bool persist_set = false;
+  if (const char* e = getenv("GC_L2_PERSIST")) {
+    int maxp = 0;
+    CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    size_t want = strtoull(e, nullptr, 10);
+    if (want == 0) want = (size_t)n * (2 + (push ? 4 : 0));
+    if (want > (size_t)maxp) want = (size_t)maxp;
+    CK(cudaDeviceGetLimit(&prev_persist, cudaLimitPersistingL2CacheSize));
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    persist_set = true;
+  }
+  struct PersistGuard {
+    bool on; size_t prev;
+    ~PersistGuard() { if (on) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev); }
+  } pg{persist_set, prev_persist};
   if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
     // ---- persistent cooperative kernel: the whole run in one launch
-    int coop = 0;
-    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    if (!coop) {
+    if (!prop.coop) {
       set_err("gc_color: device %d does not support cooperative launch", dev);
       return GC_ERR_UNSUPPORTED;
     }
-    void* fn = pick_persistent((int)o.policy, push, cw);
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0));
-    if (per_sm < 1) {
-      set_err("gc_color: persistent kernel cannot be resident");
-      return GC_ERR_UNSUPPORTED;
+    // 16-bit state words first; a vertex of degree > 32766 makes the kernel stop in its
+    // prologue with ST_NEED_WIDE and the run is repeated with 32-bit words.
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const bool narrow = attempt == 0;
+      void* fn = pick_persistent(narrow, (int)o.policy, push, cw);
+      int per_sm = 0;
+      CK(occupancy(dev, fn, &per_sm));
+      if (per_sm < 1) {
+        set_err("gc_color: persistent kernel cannot be resident");
+        return GC_ERR_UNSUPPORTED;
+      }
+      if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
+      const int grid = prop.sms * per_sm;
+      void* args[] = {&p};
+      CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s));
+      uint32_t status = 0;
+      CK(cudaMemcpyAsync(&status, &((DevInfo*)info)->status, sizeof(status), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (status != ST_NEED_WIDE) break;
+      CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
     }
-    if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
-    const int grid = prop.multiProcessorCount * per_sm;
-    void* args[] = {&p};
-    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s));
   } else {
     // ---- host-driven rounds (ablation): one launch per phase, |W| read every round
-    const int grid = prop.multiProcessorCount * 4;
+    const int grid = prop.sms * 4;
     if (push) k_prologue_count<true><<<grid, BLOCK, 0, s>>>(p);
     else k_prologue_count<false><<<grid, BLOCK, 0, s>>>(p);
     k_prologue_scatter<<<grid, BLOCK, 0, s>>>(p);
@@ -386,7 +459,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       CK(cudaMemcpyAsync(cnt, ((DevInfo*)info)->cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       const uint32_t* nx = cnt[(r + 1) % 3];
-      if (nx[0] + nx[1] + nx[2] == 0) break;
+      if (nx[0] + nx[1] + nx[2] + nx[3] == 0) break;
       if (r >= p.max_rounds) {
         set_err("gc_color: no convergence within max_rounds=%u", p.max_rounds);
         return GC_ERR_NO_CONVERGENCE;
@@ -491,19 +564,61 @@ gc_status gc_verify(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, c
   void* info;
   CK(sc.alloc(&info, sizeof(DevInfo)));
   CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, dev));
-  k_verify<<<prop.multiProcessorCount * 8, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, d_col, (DevInfo*)info);
+  DevFacts prop;
+  CK(dev_facts(dev, &prop));
+  k_verify<<<prop.sms * 8, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, d_col, (DevInfo*)info);
   CK(cudaGetLastError());
   unsigned long long bad = 0;
   CK(cudaMemcpyAsync(&bad, &((DevInfo*)info)->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (bad) {
-    *bad_vertex = (int64_t)((bad - 1) >> 3);
+    bad = ~bad;
+    *bad_vertex = (int64_t)(bad >> 3);
     set_err("gc_verify: vertex %lld violates %s", (long long)*bad_vertex,
-            ((bad - 1) & 7) == 1 ? "completeness/greedy bound" : "properness/First-Fit fixpoint");
+            (bad & 7) == 1 ? "completeness/greedy bound" : "properness/First-Fit fixpoint");
     return GC_ERR_INVALID_GRAPH;
   }
+  return GC_OK;
+}
+
+// Diagnostics (include/gc_internal.h): mean cost of one grid barrier of the persistent
+// kernel, in microseconds, for blocks_per_sm CTAs per SM (0 = max co-resident).
+gc_status gc__bench_grid_sync(int32_t device, int32_t blocks_per_sm, int32_t iters, float* us_per_sync) {
+  g_err[0] = 0;
+  if (!us_per_sync || iters < 1) return GC_ERR_INVALID_ARGUMENT;
+  Scope sc;
+  CK(cudaGetDevice(&sc.prev_dev));
+  const int dev = device >= 0 ? device : sc.prev_dev;
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+  sc.own_stream = true;
+  CK(get_pool(dev, &sc.pool));
+  DevFacts f;
+  CK(dev_facts(dev, &f));
+  void* info;
+  CK(sc.alloc(&info, sizeof(DevInfo)));
+  CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), sc.stream));
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.info = (DevInfo*)info;
+  p.timeout_ns = 10ull * 1000000000ull;
+  int per_sm = 0;
+  CK(occupancy(dev, (const void*)k_bench_sync, &per_sm));
+  if (blocks_per_sm > 0 && blocks_per_sm < per_sm) per_sm = blocks_per_sm;
+  void* args[] = {&p, &iters};
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaLaunchCooperativeKernel((void*)k_bench_sync, dim3(f.sms * per_sm), dim3(BLOCK), args, 0, sc.stream));
+  CK(cudaEventRecord(a, sc.stream));
+  CK(cudaLaunchCooperativeKernel((void*)k_bench_sync, dim3(f.sms * per_sm), dim3(BLOCK), args, 0, sc.stream));
+  CK(cudaEventRecord(b, sc.stream));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us_per_sync = ms * 1000.f / iters;
   return GC_OK;
 }
 

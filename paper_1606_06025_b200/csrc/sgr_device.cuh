@@ -1,30 +1,33 @@
-// sgr_device.cuh — device side of the round-synchronous SGR colouring path (sm_100a).
+// sgr_device.cuh — device building blocks of the round-synchronous SGR colouring path
+// (sm_100a).  See sgr_kernels.cuh for the phases and DESIGN.md §5 for the design.
 //
 // Paper mapping (arXiv 1606.06025, /root/reference/PAPER.md):
 //   Phase A  = FirstFit (Alg. 4) with the bitset + find-first-set refinement
 //              (§3.2 "Bitset Operation");
-//   Phase B  = ConflictResolve (Alg. 5) fused with the W_out push and prefix /
-//              aggregated atomics (§3.1 "Atomic Operation Reduction");
-//   rounds   = Data-GC (Alg. 7) with double-buffered worklists in
-//              ONE persistent kernel with a device-wide barrier (§3.3 "Kernel Fusion",
-//              P:653-667) — no host involvement per round;
-//   binning  = thread / warp / CTA per vertex by degree (§3.3 "Load Balancing");
-//   CSR read through the read-only path (§3.3 "Read-only Data Caching").
+//   Phase B  = ConflictResolve (Alg. 5) fused with the W_out push and aggregated
+//              atomics (§3.1 "Atomic Operation Reduction");
+//   rounds   = Data-GC (Alg. 7), double-buffered worklists, ONE
+//              persistent kernel with a device-wide barrier (§3.3 "Kernel Fusion");
+//   binning  = thread / 8-lane group / warp / CTA per vertex by degree (§3.3 "Load
+//              Balancing");
+//   CSR read through the non-coherent read-only path (§3.3 "Read-only Data Caching").
 //
-// B200-first differences from the paper's K40c design (DESIGN.md §5):
+// B200-first differences from the paper's K40c design:
 //   * Jacobi rounds (north star): Phase A uses only colours committed before the round,
-//     Phase B uses the round's tentative colours; the result is schedule independent.
-//   * One 32-bit state word per vertex: bit31 = committed, bits 0..30 = colour (tentative
-//     while bit31 = 0).  Phase A only USES committed words and only writes pending ones;
-//     Phase B only reads colour bits and only sets bit31 — so neither phase ever uses a
-//     bit that is being written in the same phase (aligned 32-bit words are single-copy
-//     atomic), and no locks are needed.
-//   * Incremental forbidden-colour mask (default): committed colours never change, so a
-//     vertex's forbidden set only grows.  A committing vertex ORs its colour bit
-//     (colours 1..32) into fm[w] of every neighbour (one RED per directed edge over the
-//     whole run).  Phase A is then O(1): tent = ffs(~fm[v]); only when colours 1..32 are
-//     all forbidden does it fall back to the exact windowed neighbour scan from colour 33.
+//     Phase B the round's tentative colours; the result is schedule independent.
+//   * One state word per vertex, S = uint16_t when Delta+1 <= 32767 (else uint32_t): top bit
+//     = committed, the rest = colour (tentative while the top bit is clear).  Phase A only
+//     USES committed words and only writes pending ones; Phase B only reads colour bits and
+//     only sets the top bit of its own vertex — so no phase uses a bit written in the same
+//     phase (aligned words are single-copy atomic) and no locks are needed.  16-bit words
+//     halve the gather footprint so it stays resident in the 126 MB L2.
+//   * Incremental forbidden-colour mask fm[v] (colours 1..32): committed colours never
+//     change, so a committing vertex REDs its colour bit into fm of every neighbour (one RED
+//     per directed edge over the whole run) and Phase A is O(1): tent = ffs(~fm[v]); only a
+//     full mask falls back to the exact windowed scan from colour 33 (reading C7).
 //     GC_FLAG_PULL_FIRSTFIT selects the paper's full rescan instead (same result).
+//   * L2 eviction priorities: the per-vertex state (st, fm) is loaded/stored evict_last,
+//     the streamed CSR and worklists evict_first.
 //   * Round 1 needs no Phase A: nothing is committed, so every tentative colour is 1.
 #pragma once
 #include <cuda_runtime.h>
@@ -32,16 +35,25 @@
 
 namespace gcdev {
 
-constexpr uint32_t COMMIT = 0x80000000u;
-constexpr uint32_t CMASK = 0x7fffffffu;
-constexpr int NBIN = 3;            // 0 = thread, 1 = warp, 2 = CTA per vertex
+constexpr int NBIN = 4;            // 0 = thread, 1 = 8-lane group, 2 = warp, 3 = CTA per vertex
+constexpr int PBUF = 64;           // per-warp push staging entries per bin
 constexpr int BLOCK = 256;
 constexpr int WARPS = BLOCK / 32;
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int32_t NARROW_MAX_DEG = 32766;  // 16-bit state: colours <= Delta+1 <= 32767
 
 enum Policy { HIGHER_ID = 0, LOWER_ID = 1, DEGREE = 2 };
-enum Status { ST_OK = 0, ST_NO_CONVERGENCE = 3, ST_WATCHDOG = 5 };
+enum Status { ST_OK = 0, ST_NEED_WIDE = 2, ST_NO_CONVERGENCE = 3, ST_WATCHDOG = 5 };
 enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_N };
+
+// State-word traits: top bit = committed, remaining bits = colour.
+template <class S> struct SW;
+template <> struct SW<uint16_t> {
+  static constexpr uint32_t COMMIT = 0x8000u, CMASK = 0x7fffu;
+};
+template <> struct SW<uint32_t> {
+  static constexpr uint32_t COMMIT = 0x80000000u, CMASK = 0x7fffffffu;
+};
 
 // Device-side run state.  Zeroed by the host before launch.
 struct DevInfo {
@@ -52,10 +64,12 @@ struct DevInfo {
   uint32_t binsize[NBIN];
   uint32_t cursor[NBIN];
   uint32_t cnt[3][NBIN];        // |W| per bin, triple-buffered by round (r % 3)
-  uint32_t pad1[13];
+  uint32_t pad1[8];
+  uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
+  unsigned long long wlp[2];    // the two worklist buffers (re-read every round, see sgr_persistent)
   unsigned long long work[W_N];
-  unsigned long long bad;       // validation / verify: first offending index + 1 (min)
-  uint32_t err_code;            // validation error kind
+  unsigned long long bad;       // validation / verify: ~(smallest offending key), 0 = none
+  uint32_t err_code;
   uint32_t pad2[31];
   uint32_t bar_count;           // grid barrier (own 128-B lines)
   uint32_t pad3[31];
@@ -67,7 +81,7 @@ struct Params {
   int32_t n;
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;
-  uint32_t* st;                 // state word per vertex
+  void* st;                     // state word per vertex (uint16_t or uint32_t)
   uint32_t* fm;                 // forbidden colours 1..32 per vertex (incremental mode)
   int32_t* wl0;                 // worklist buffers, n entries each, bin segments
   int32_t* wl1;
@@ -76,33 +90,87 @@ struct Params {
   uint32_t trace_cap;
   uint32_t* colors_out;
   uint32_t max_rounds;
-  uint32_t tb;                  // thread-bin max degree
-  uint32_t wb;                  // warp-bin max degree
+  uint32_t t1;                  // degree <= t1: one thread per vertex
+  uint32_t t2;                  // degree <= t2: one 8-lane group per vertex
+  uint32_t t3;                  // degree <= t3: one warp per vertex; above: one CTA
   unsigned long long timeout_ns;
 };
 
 struct Work {
   unsigned long long v[W_N];
-  __device__ void zero() {
+  __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int i = 0; i < W_N; ++i) v[i] = 0;
   }
 };
 
 // ---------------------------------------------------------------- memory helpers
+// L2 eviction-priority policies (createpolicy, sm_80+).
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// CSR: read-only for the whole kernel (non-coherent path), streamed (evict_first).
+__device__ __forceinline__ int32_t ldc(const int32_t* __restrict__ p, int64_t i) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p + i), "l"(pol_first()));
   return v;
 }
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ int64_t ldr(const int64_t* __restrict__ p, int64_t i) {
+  int64_t v;
+  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p + i), "l"(pol_first()));
+  return v;
+}
+// Worklists: written in one phase, read after a barrier (coherent loads), streamed.
+__device__ __forceinline__ int32_t ldw(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_first()) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stw(int32_t* p, int32_t v) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol_first()) : "memory");
+}
+// Per-vertex state: kept resident (evict_last).
+__device__ __forceinline__ uint32_t lds(const uint16_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol_last()) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_last()) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint16_t* p, uint32_t v) {
+  asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(p), "h"((uint16_t)v), "l"(pol_last()) : "memory");
+}
+__device__ __forceinline__ void sts(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol_last()) : "memory");
+}
+__device__ __forceinline__ uint32_t ldf(const uint32_t* p) { return lds(p); }
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t bit) {
+  asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(bit), "l"(pol_last()) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -114,84 +182,145 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-// CSR is read-only for the whole kernel: non-coherent read-only path.
-__device__ __forceinline__ int32_t ldc(const int32_t* __restrict__ p, int64_t i) { return __ldg(p + i); }
-__device__ __forceinline__ int64_t ldr(const int64_t* __restrict__ p, int64_t i) { return __ldg(p + i); }
-// Colour of a state word.
-__device__ __forceinline__ uint32_t color_of(uint32_t s) { return s & CMASK; }
 
 // ---------------------------------------------------------------- grid barrier
-// Sense (generation) barrier over all co-resident CTAs of the cooperative launch, with a
-// globaltimer watchdog so that a bug can never hang the GPU: on timeout the status becomes
-// ST_WATCHDOG and every CTA leaves at its next barrier.  Returns false when the run must
-// stop.  Release/acquire at gpu scope order every write of the phase before every read of
-// the next phase (and invalidate stale L1 lines).
-__device__ __forceinline__ bool grid_sync(const Params& p) {
+// Generation barrier over all co-resident CTAs of the cooperative launch.  The arriving
+// CTA publishes its phase with a fence + relaxed atomic; waiters spin on RELAXED loads (an
+// acquire load per iteration would invalidate L1 each time, also evicting the L1 lines of
+// the other CTAs still working on this SM) and fence once when the generation flips.
+// A globaltimer watchdog turns any bug into an error status instead of a hung GPU.
+// Returns false when the run must stop.  Deliberately NOT inlined: with the barrier inlined
+// into the round loop, ptxas 12.9 was observed to reuse a live uniform register (holding a
+// worklist base pointer) as scratch for the barrier address (truncated-pointer faults).
+__device__ __noinline__ bool grid_sync(const Params& p) {
   __syncthreads();
   if (threadIdx.x == 0) {
     DevInfo* I = p.info;
-    const uint32_t gen = ld_acquire(&I->bar_gen);
+    const uint32_t gen = ld_relaxed(&I->bar_gen);
     __threadfence();
     const uint32_t arrived = atomicAdd(&I->bar_count, 1u);
     if (arrived == gridDim.x - 1) {
       atomicExch(&I->bar_count, 0u);
-      __threadfence();
       st_release(&I->bar_gen, gen + 1);
     } else {
       const unsigned long long t0 = globaltimer();
-      while (ld_acquire(&I->bar_gen) == gen) {
-        __nanosleep(32);
+      while (ld_relaxed(&I->bar_gen) == gen) {
+        __nanosleep(64);
         if (globaltimer() - t0 > p.timeout_ns) {
           atomicExch(&I->status, (uint32_t)ST_WATCHDOG);
           break;
         }
       }
     }
+    __threadfence();  // acquire side: orders the next phase's reads after the flip
   }
   __syncthreads();
-  return ld_relaxed(&p.info->status) != ST_WATCHDOG;
+  return ld_relaxed(&p.info->status) == ST_OK;
 }
 
 // ---------------------------------------------------------------- bins
 
 __device__ __forceinline__ int bin_of(const Params& p, int64_t deg) {
-  return deg <= (int64_t)p.tb ? 0 : (deg <= (int64_t)p.wb ? 1 : 2);
+  return deg <= (int64_t)p.t1 ? 0 : deg <= (int64_t)p.t2 ? 1 : deg <= (int64_t)p.t3 ? 2 : 3;
 }
 
+// Offsets of the bin segments inside each worklist buffer (fixed for the whole run).
 struct Bins {
   uint32_t off[NBIN];
-  __device__ void load(const Params& p) {
-    uint32_t b0 = ld_relaxed(&p.info->binsize[0]), b1 = ld_relaxed(&p.info->binsize[1]);
-    off[0] = 0;
-    off[1] = b0;
-    off[2] = b0 + b1;
+  __device__ __forceinline__ void load(const Params& p) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int b = 0; b < NBIN; ++b) {
+      off[b] = acc;
+      acc += ld_relaxed(&p.info->binsize[b]);
+    }
+  }
+};
+
+// Per-warp staging of W_out pushes (§3.1 "Atomic Operation Reduction"): losers
+// are appended to a 64-entry shared-memory buffer per bin and written out 32 at a time
+// with ONE global atomic per 32 pushes (coalesced 128-B stores); remainders are flushed at
+// the end of the phase.  Counts are warp-uniform registers.
+struct Pusher {
+  int32_t* buf;            // this warp's [NBIN][PBUF] staging area (shared memory)
+  int32_t* out;            // W_out
+  uint32_t* gcnt;          // &info->cnt[next][0]
+  uint32_t off[NBIN];
+  uint32_t c[NBIN];
+  __device__ __forceinline__ void init(int32_t* b, int32_t* o, uint32_t* g, const Bins& bins) {
+    buf = b;
+    out = o;
+    gcnt = g;
+#pragma unroll
+    for (int k = 0; k < NBIN; ++k) { off[k] = bins.off[k]; c[k] = 0; }
+  }
+  template <int B, bool CW>
+  __device__ __forceinline__ void push(bool pred, int32_t v, int lane, unsigned long long& pushed) {
+    const unsigned m = __ballot_sync(FULL, pred);
+    if (!m) return;
+    int32_t* bb = buf + B * PBUF;
+    if (pred) bb[c[B] + __popc(m & lanemask_lt())] = v;
+    c[B] += __popc(m);
+    if (c[B] >= 32) {
+      __syncwarp();
+      uint32_t pos = 0;
+      if (lane == 0) pos = atomicAdd(&gcnt[B], 32u);
+      pos = __shfl_sync(FULL, pos, 0);
+      stw(out + off[B] + pos + lane, bb[lane]);
+      const uint32_t rest = c[B] - 32;
+      const int32_t x = (uint32_t)lane < rest ? bb[32 + lane] : 0;
+      __syncwarp();
+      if ((uint32_t)lane < rest) bb[lane] = x;
+      __syncwarp();
+      c[B] = rest;
+      if (CW && lane == 0) pushed += 32;
+    }
+  }
+  template <int B, bool CW>
+  __device__ __forceinline__ void flush_bin(int lane, unsigned long long& pushed) {
+    if (!c[B]) return;
+    __syncwarp();
+    uint32_t pos = 0;
+    if (lane == 0) pos = atomicAdd(&gcnt[B], c[B]);
+    pos = __shfl_sync(FULL, pos, 0);
+    if ((uint32_t)lane < c[B]) stw(out + off[B] + pos + lane, buf[B * PBUF + lane]);
+    if (CW && lane == 0) pushed += c[B];
+    __syncwarp();
+    c[B] = 0;
+  }
+  template <bool CW>
+  __device__ __forceinline__ void flush(int lane, unsigned long long& pushed) {
+    flush_bin<0, CW>(lane, pushed);
+    flush_bin<1, CW>(lane, pushed);
+    flush_bin<2, CW>(lane, pushed);
   }
 };
 
 // ---------------------------------------------------------------- First-Fit (Phase A)
+// Exact windowed First-Fit (reading C7): smallest colour >= base absent from the colours of
+// the committed neighbours, 64 colours per window.
 
-// Exact windowed First-Fit over committed neighbours, one thread (reading C7):
-// smallest colour >= base absent from the committed neighbour colours.
-template <bool CW>
-__device__ uint32_t firstfit_thread(const Params& p, int32_t v, uint32_t base, Work& wk) {
+template <class S, bool CW>
+__device__ __forceinline__ uint32_t firstfit_thread(const Params& p, int32_t v, uint32_t base, Work& wk) {
+  const S* st = (const S*)p.st;
   const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
   for (;;) {
     unsigned long long mask = 0;
     int64_t e = beg;
     for (; e + 4 <= end; e += 4) {
       const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + 1), w2 = ldc(p.ci, e + 2), w3 = ldc(p.ci, e + 3);
-      const uint32_t s0 = p.st[w0], s1 = p.st[w1], s2 = p.st[w2], s3 = p.st[w3];
-      const uint32_t d0 = color_of(s0) - base, d1 = color_of(s1) - base;
-      const uint32_t d2 = color_of(s2) - base, d3 = color_of(s3) - base;
-      if ((s0 & COMMIT) && d0 < 64) mask |= 1ull << d0;
-      if ((s1 & COMMIT) && d1 < 64) mask |= 1ull << d1;
-      if ((s2 & COMMIT) && d2 < 64) mask |= 1ull << d2;
-      if ((s3 & COMMIT) && d3 < 64) mask |= 1ull << d3;
+      const uint32_t s0 = lds(st + w0), s1 = lds(st + w1), s2 = lds(st + w2), s3 = lds(st + w3);
+      const uint32_t d0 = (s0 & SW<S>::CMASK) - base, d1 = (s1 & SW<S>::CMASK) - base;
+      const uint32_t d2 = (s2 & SW<S>::CMASK) - base, d3 = (s3 & SW<S>::CMASK) - base;
+      if ((s0 & SW<S>::COMMIT) && d0 < 64) mask |= 1ull << d0;
+      if ((s1 & SW<S>::COMMIT) && d1 < 64) mask |= 1ull << d1;
+      if ((s2 & SW<S>::COMMIT) && d2 < 64) mask |= 1ull << d2;
+      if ((s3 & SW<S>::COMMIT) && d3 < 64) mask |= 1ull << d3;
     }
     for (; e < end; ++e) {
-      const uint32_t s = p.st[ldc(p.ci, e)];
-      const uint32_t d = color_of(s) - base;
-      if ((s & COMMIT) && d < 64) mask |= 1ull << d;
+      const uint32_t s = lds(st + ldc(p.ci, e));
+      const uint32_t d = (s & SW<S>::CMASK) - base;
+      if ((s & SW<S>::COMMIT) && d < 64) mask |= 1ull << d;
     }
     if (CW) wk.v[W_A_EDGE] += (unsigned long long)(end - beg);
     if (~mask) return base + (uint32_t)__ffsll((long long)~mask) - 1;
@@ -199,17 +328,16 @@ __device__ uint32_t firstfit_thread(const Params& p, int32_t v, uint32_t base, W
   }
 }
 
-// Same, one warp per vertex; lanes stride over the row (coalesced 128-B col_idx reads),
-// per-lane window bits combined with __reduce_or_sync, smallest free bit with __ffs.
-template <bool CW>
-__device__ uint32_t firstfit_warp(const Params& p, int32_t v, uint32_t base, Work& wk, int lane) {
+template <class S, bool CW>
+__device__ __forceinline__ uint32_t firstfit_warp(const Params& p, int32_t v, uint32_t base, Work& wk, int lane) {
+  const S* st = (const S*)p.st;
   const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
   for (;;) {
     uint32_t lo = 0, hi = 0;
     for (int64_t e = beg + lane; e < end; e += 32) {
-      const uint32_t s = p.st[ldc(p.ci, e)];
-      const uint32_t d = color_of(s) - base;
-      if (s & COMMIT) {
+      const uint32_t s = lds(st + ldc(p.ci, e));
+      const uint32_t d = (s & SW<S>::CMASK) - base;
+      if (s & SW<S>::COMMIT) {
         if (d < 32) lo |= 1u << d;
         else if (d < 64) hi |= 1u << (d - 32);
       }
@@ -223,18 +351,18 @@ __device__ uint32_t firstfit_warp(const Params& p, int32_t v, uint32_t base, Wor
   }
 }
 
-// Same, one CTA per vertex; window bits in shared memory.
-template <bool CW>
-__device__ uint32_t firstfit_cta(const Params& p, int32_t v, uint32_t base, Work& wk, uint32_t* s_win) {
+template <class S, bool CW>
+__device__ __forceinline__ uint32_t firstfit_cta(const Params& p, int32_t v, uint32_t base, Work& wk, uint32_t* s_win) {
+  const S* st = (const S*)p.st;
   const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
   for (;;) {
     if (threadIdx.x < 2) s_win[threadIdx.x] = 0;
     __syncthreads();
     uint32_t lo = 0, hi = 0;
     for (int64_t e = beg + threadIdx.x; e < end; e += BLOCK) {
-      const uint32_t s = p.st[ldc(p.ci, e)];
-      const uint32_t d = color_of(s) - base;
-      if (s & COMMIT) {
+      const uint32_t s = lds(st + ldc(p.ci, e));
+      const uint32_t d = (s & SW<S>::CMASK) - base;
+      if (s & SW<S>::COMMIT) {
         if (d < 32) lo |= 1u << d;
         else if (d < 64) hi |= 1u << (d - 32);
       }
@@ -270,19 +398,23 @@ __device__ __forceinline__ bool recolors(const Params& p, int32_t v, int32_t w, 
 // ---------------------------------------------------------------- Phase B scans
 // Each returns true when v must recolour (is pushed to W_out).  HIGHER_ID only needs the
 // lower-id prefix of the (sorted) row and stops at the first w > v or the first hit;
-// LOWER_ID scans the upper suffix from the end; DEGREE scans the whole row.
+// LOWER_ID scans the upper suffix from the end; DEGREE scans the whole row.  Work counters
+// (CW) follow the sequential scan, whatever the lane mapping.
 
-template <int POL, bool CW>
-__device__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end, Work& wk) {
+template <class S, int POL, bool CW>
+__device__ __forceinline__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end,
+                                                Work& wk) {
+  const S* st = (const S*)p.st;
+  constexpr uint32_t CM = SW<S>::CMASK;
   if (POL == HIGHER_ID) {
     int64_t e = beg;
     for (; e + 4 <= end; e += 4) {
       const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + 1), w2 = ldc(p.ci, e + 2), w3 = ldc(p.ci, e + 3);
       // speculative gathers of the lower-id candidates (rows are sorted: w0<w1<w2<w3)
-      const uint32_t c0 = w0 < v ? color_of(p.st[w0]) : 0u;
-      const uint32_t c1 = w1 < v ? color_of(p.st[w1]) : 0u;
-      const uint32_t c2 = w2 < v ? color_of(p.st[w2]) : 0u;
-      const uint32_t c3 = w3 < v ? color_of(p.st[w3]) : 0u;
+      const uint32_t c0 = w0 < v ? (lds(st + w0) & CM) : 0u;
+      const uint32_t c1 = w1 < v ? (lds(st + w1) & CM) : 0u;
+      const uint32_t c2 = w2 < v ? (lds(st + w2) & CM) : 0u;
+      const uint32_t c3 = w3 < v ? (lds(st + w3) & CM) : 0u;
       if (w0 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 1; wk.v[W_B_GATHER] += e - beg; } return false; }
       if (c0 == tent) { if (CW) { wk.v[W_B_EDGE] += e - beg + 1; wk.v[W_B_GATHER] += e - beg + 1; } return true; }
       if (w1 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 2; wk.v[W_B_GATHER] += e - beg + 1; } return false; }
@@ -297,7 +429,7 @@ __device__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64
       if (CW) wk.v[W_B_EDGE] += 1;
       if (w > v) return false;
       if (CW) wk.v[W_B_GATHER] += 1;
-      if (color_of(p.st[w]) == tent) return true;
+      if ((lds(st + w) & CM) == tent) return true;
     }
     return false;
   } else if (POL == LOWER_ID) {
@@ -306,7 +438,7 @@ __device__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64
       if (CW) wk.v[W_B_EDGE] += 1;
       if (w < v) return false;
       if (CW) wk.v[W_B_GATHER] += 1;
-      if (color_of(p.st[w]) == tent) return true;
+      if ((lds(st + w) & CM) == tent) return true;
     }
     return false;
   } else {
@@ -314,44 +446,64 @@ __device__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64
     for (int64_t e = beg; e < end; ++e) {
       const int32_t w = ldc(p.ci, e);
       if (CW) { wk.v[W_B_EDGE] += 1; wk.v[W_B_GATHER] += 1; }
-      if (color_of(p.st[w]) == tent && recolors<DEGREE>(p, v, w, dv)) return true;
+      if ((lds(st + w) & CM) == tent && recolors<DEGREE>(p, v, w, dv)) return true;
     }
     return false;
   }
 }
 
-// Warp scan: 32 row entries per step; the step stops the scan if any lane hits or (for the
-// id policies) reaches the other side of v.  Work counters follow the sequential scan.
-template <int POL, bool CW>
-__device__ bool conflict_warp(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end, Work& wk, int lane) {
+// Group scan: a group of G lanes (G = 8 or 32, aligned in the warp) examines its vertex's row
+// G entries per step.  Called by the whole warp in lockstep (warp-uniform loop); inactive
+// groups pass act = false.  Returns the group's verdict in every lane of the group.
+template <class S, int G, int POL, bool CW>
+__device__ __forceinline__ bool conflict_group(const Params& p, bool act, int32_t v, uint32_t tent, int64_t beg,
+                                               int64_t end, int lane, Work& wk) {
+  const S* st = (const S*)p.st;
+  const int gl = lane % G;
+  const int shift = (lane / G) * G;
+  const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << shift);
+  const int64_t len = act ? end - beg : 0;
   const int64_t dv = end - beg;
-  const int64_t len = end - beg;
-  for (int64_t k = 0; k < len; k += 32) {
-    const int64_t j = k + lane;
-    const bool valid = j < len;
-    const int64_t e = (POL == LOWER_ID) ? end - 1 - j : beg + j;
-    const int32_t w = valid ? ldc(p.ci, e) : v;
-    bool side, hit = false;
-    if (POL == HIGHER_ID) side = valid && w < v;
-    else if (POL == LOWER_ID) side = valid && w > v;
-    else side = valid;
-    if (side) hit = color_of(p.st[w]) == tent && recolors<POL>(p, v, w, dv);
-    const unsigned stop = __ballot_sync(FULL, hit || !side);
-    if (CW) {
-      // sequential-scan counters: entries / gathers up to and including the stop lane
-      const int kk = stop ? __ffs(stop) - 1 : 31;
-      const unsigned ev = __ballot_sync(FULL, valid && lane <= kk);
-      const unsigned g = __ballot_sync(FULL, side && lane <= kk);
-      if (lane == 0) { wk.v[W_B_EDGE] += __popc(ev); wk.v[W_B_GATHER] += __popc(g); }
+  bool done = len == 0;
+  bool lose = false;
+  for (int64_t k = 0;; k += G) {
+    if (__all_sync(FULL, done)) break;
+    bool hit = false, stop = false, side = false, valid = false;
+    if (!done) {
+      const int64_t j = k + gl;
+      valid = j < len;
+      const int64_t e = (POL == LOWER_ID) ? end - 1 - j : beg + j;
+      const int32_t w = valid ? ldc(p.ci, e) : v;
+      if (POL == HIGHER_ID) side = valid && w < v;
+      else if (POL == LOWER_ID) side = valid && w > v;
+      else side = valid;
+      if (side) hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
+      stop = hit || !side;
     }
-    if (__any_sync(FULL, hit)) return true;
-    if (stop) return false;
+    const unsigned hb = __ballot_sync(FULL, hit) & gmask;
+    const unsigned sb = __ballot_sync(FULL, stop) & gmask;
+    if (CW) {
+      const unsigned vb = __ballot_sync(FULL, valid) & gmask;
+      const unsigned db = __ballot_sync(FULL, side) & gmask;
+      if (!done && gl == 0) {
+        const int f = sb ? __ffs(sb >> shift) - 1 : G - 1;  // the sequential scan stops here
+        const unsigned upto = (f >= 31 ? FULL : ((2u << f) - 1u)) << shift;
+        wk.v[W_B_EDGE] += __popc(vb & upto);
+        wk.v[W_B_GATHER] += __popc(db & upto);
+      }
+    }
+    if (!done) {
+      if (hb) { lose = true; done = true; }
+      else if (sb || k + G >= len) done = true;
+    }
   }
-  return false;
+  return lose;
 }
 
-template <int POL, bool CW>
-__device__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end, Work& wk) {
+template <class S, int POL, bool CW>
+__device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end,
+                                             Work& wk, int* s_first) {
+  const S* st = (const S*)p.st;
   const int64_t dv = end - beg;
   const int64_t len = end - beg;
   for (int64_t k = 0; k < len; k += BLOCK) {
@@ -363,19 +515,15 @@ __device__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t 
     if (POL == HIGHER_ID) side = valid && w < v;
     else if (POL == LOWER_ID) side = valid && w > v;
     else side = valid;
-    if (side) hit = color_of(p.st[w]) == tent && recolors<POL>(p, v, w, dv);
+    if (side) hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
     if (CW) {
-      // sequential-scan counters: entries up to the first stopping position
-      __shared__ int s_first;
-      if (threadIdx.x == 0) s_first = BLOCK;
+      if (threadIdx.x == 0) *s_first = BLOCK;
       __syncthreads();
-      if (hit || !side) atomicMin(&s_first, (int)threadIdx.x);
+      if (hit || !side) atomicMin(s_first, (int)threadIdx.x);
       __syncthreads();
-      const int kk = s_first < BLOCK ? s_first : BLOCK - 1;
-      const bool counted_edge = valid && (int)threadIdx.x <= kk;
-      const bool counted_gather = side && (int)threadIdx.x <= kk;
-      const int ne = __syncthreads_count(counted_edge);
-      const int ng = __syncthreads_count(counted_gather);
+      const int kk = *s_first < BLOCK ? *s_first : BLOCK - 1;
+      const int ne = __syncthreads_count(valid && (int)threadIdx.x <= kk);
+      const int ng = __syncthreads_count(side && (int)threadIdx.x <= kk);
       if (threadIdx.x == 0) { wk.v[W_B_EDGE] += ne; wk.v[W_B_GATHER] += ng; }
     }
     if (__syncthreads_or(hit)) return true;
@@ -385,9 +533,20 @@ __device__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t 
 }
 
 // ---------------------------------------------------------------- commit scatter
-// A winner ORs its colour bit into every neighbour's forbidden mask (incremental mode).
-__device__ __forceinline__ void scatter_thread(const Params& p, uint32_t bit, int64_t beg, int64_t end) {
-  for (int64_t e = beg; e < end; ++e) atomicOr(&p.fm[ldc(p.ci, e)], bit);
+// A winner ORs its colour bit into the forbidden mask of every neighbour: entries
+// e = start, start+STEP, ... < end; four col_idx loads are issued before the four
+// fire-and-forget REDs so that each lane keeps several misses in flight.
+template <int STEP>
+__device__ __forceinline__ void scatter(const Params& p, uint32_t bit, int64_t start, int64_t end) {
+  int64_t e = start;
+  for (; e + 3 * STEP < end; e += 4 * STEP) {
+    const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + STEP), w2 = ldc(p.ci, e + 2 * STEP), w3 = ldc(p.ci, e + 3 * STEP);
+    red_or(p.fm + w0, bit);
+    red_or(p.fm + w1, bit);
+    red_or(p.fm + w2, bit);
+    red_or(p.fm + w3, bit);
+  }
+  for (; e < end; e += STEP) red_or(p.fm + ldc(p.ci, e), bit);
 }
 
 }  // namespace gcdev

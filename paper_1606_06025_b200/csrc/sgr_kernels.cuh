@@ -1,6 +1,8 @@
 // sgr_kernels.cuh — phases and kernels of the SGR colouring path (sm_100a).
 // Phase functions are shared by the persistent cooperative kernel (default) and by the
 // one-launch-per-phase host-driven ablation (GC_FLAG_HOST_ROUNDS).
+// Template parameters: S = state word (uint16_t / uint32_t), POL = conflict policy,
+// PUSH = incremental forbidden masks (else full rescans), CW = exact work counters.
 #pragma once
 #include "sgr_device.cuh"
 
@@ -8,22 +10,27 @@ namespace gcdev {
 
 // ---------------------------------------------------------------- a1: ingest + bins
 // P0: degrees -> bin sizes; st[v] = 1 (round-1 tentative colour: nothing is committed yet,
-// so First-Fit gives 1 to every vertex), fm[v] = 0.
-template <bool PUSH>
-__device__ void prologue_count(const Params& p) {
+// so First-Fit gives 1 to every vertex), fm[v] = 0.  With 16-bit state words a vertex of
+// degree > NARROW_MAX_DEG makes the run restart with 32-bit words (ST_NEED_WIDE).
+template <class S, bool PUSH>
+__device__ __forceinline__ void prologue_count(const Params& p) {
   __shared__ uint32_t s_cnt[NBIN];
   if (threadIdx.x < NBIN) s_cnt[threadIdx.x] = 0;
   __syncthreads();
+  S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
+  bool wide = false;
   for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
     int b = -1;
     if (act) {
-      b = bin_of(p, ldr(p.rp, v + 1) - ldr(p.rp, v));
-      p.st[v] = 1u;
-      if (PUSH) p.fm[v] = 0u;
+      const int64_t deg = ldr(p.rp, v + 1) - ldr(p.rp, v);
+      if (sizeof(S) == 2 && deg > NARROW_MAX_DEG) wide = true;
+      b = bin_of(p, deg);
+      sts(st + v, 1u);
+      if (PUSH) sts(p.fm + v, 0u);
     }
 #pragma unroll
     for (int k = 0; k < NBIN; ++k) {
@@ -31,13 +38,18 @@ __device__ void prologue_count(const Params& p) {
       if (m && lane == 0) atomicAdd(&s_cnt[k], (uint32_t)__popc(m));
     }
   }
+  if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED_WIDE);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.info->wlp[0] = (unsigned long long)p.wl0;
+    p.info->wlp[1] = (unsigned long long)p.wl1;
+  }
   __syncthreads();
   if (threadIdx.x < NBIN && s_cnt[threadIdx.x]) atomicAdd(&p.info->binsize[threadIdx.x], s_cnt[threadIdx.x]);
 }
 
 // P1: W_1 = V, split into bin segments of wl0 (warp-aggregated cursors; order within a
 // bin is free, reading C12).
-__device__ void prologue_scatter(const Params& p, const Bins& bins) {
+__device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bins) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
@@ -52,164 +64,221 @@ __device__ void prologue_scatter(const Params& p, const Bins& bins) {
       uint32_t pos = 0;
       if (lane == leader) pos = atomicAdd(&p.info->cursor[k], (uint32_t)__popc(m));
       pos = __shfl_sync(FULL, pos, leader);
-      if (b == k) p.wl0[bins.off[k] + pos + __popc(m & lanemask_lt())] = (int32_t)v;
+      if (b == k) stw(p.wl0 + bins.off[k] + pos + __popc(m & lanemask_lt()), (int32_t)v);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = p.info->binsize[threadIdx.x];
 }
 
 // ---------------------------------------------------------------- a2: Phase A
-template <bool PUSH, bool CW>
-__device__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, Work& wk) {
-  __shared__ uint32_t s_win[2];
-  const uint32_t cur = r % 3;
-  const uint32_t nT = ld_relaxed(&p.info->cnt[cur][0]);
-  const uint32_t nW = ld_relaxed(&p.info->cnt[cur][1]);
-  const uint32_t nC = ld_relaxed(&p.info->cnt[cur][2]);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // reset the counters round r+1 will push into (last read in round r-2)
-  if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
-  if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nT + nW + nC;
-
-  // thread bin
-  {
-    const int32_t* Wb = W + bins.off[0];
-    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nT; i += gridDim.x * BLOCK) {
-      const int32_t v = Wb[i];
-      uint32_t tent;
-      if (PUSH) {
-        const uint32_t f = p.fm[v];
-        tent = (f != FULL) ? (uint32_t)__ffs(~f) : firstfit_thread<CW>(p, v, 33u, wk);
-      } else {
-        tent = firstfit_thread<CW>(p, v, 1u, wk);
+// Incremental-mask mode: every pending vertex is O(1) (tent = ffs(~fm[v])), so all bins are
+// processed thread-per-vertex; a vertex whose 32-colour mask is full is handed to the whole
+// warp, which runs the exact windowed First-Fit from colour 33 (reading C7).
+template <class S, bool CW>
+__device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, const int32_t* W, const uint32_t* nb,
+                                             Work& wk) {
+  S* st = (S*)p.st;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
+#pragma unroll
+  for (int b = 0; b < NBIN; ++b) {
+    const int32_t* Wb = W + bins.off[b];
+    const uint32_t cnt = nb[b];
+    for (uint32_t base = gw * 32; base < cnt; base += nw * 32) {
+      const uint32_t i = base + lane;
+      const bool act = i < cnt;
+      int32_t v = 0;
+      uint32_t f = 0;
+      if (act) {
+        v = ldw(Wb + i);
+        f = ldf(p.fm + v);
       }
-      p.st[v] = tent;
-    }
-  }
-  // warp bin
-  {
-    const int32_t* Wb = W + bins.off[1];
-    const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-    for (uint32_t i = gw; i < nW; i += nw) {
-      const int32_t v = Wb[i];
-      uint32_t tent;
-      if (PUSH) {
-        const uint32_t f = p.fm[v];
-        tent = (f != FULL) ? (uint32_t)__ffs(~f) : firstfit_warp<CW>(p, v, 33u, wk, lane);
-      } else {
-        tent = firstfit_warp<CW>(p, v, 1u, wk, lane);
+      const bool fb = act && f == FULL;
+      if (act && !fb) sts(st + v, (uint32_t)__ffs(~f));
+      unsigned m = __ballot_sync(FULL, fb);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t u = __shfl_sync(FULL, v, src);
+        const uint32_t t = firstfit_warp<S, CW>(p, u, 33u, wk, lane);
+        if (lane == 0) sts(st + u, t);
       }
-      if (lane == 0) p.st[v] = tent;
-    }
-  }
-  // CTA bin
-  {
-    const int32_t* Wb = W + bins.off[2];
-    for (uint32_t i = blockIdx.x; i < nC; i += gridDim.x) {
-      const int32_t v = Wb[i];
-      uint32_t tent;
-      if (PUSH) {
-        const uint32_t f = p.fm[v];
-        tent = (f != FULL) ? (uint32_t)__ffs(~f) : firstfit_cta<CW>(p, v, 33u, wk, s_win);
-      } else {
-        tent = firstfit_cta<CW>(p, v, 1u, wk, s_win);
-      }
-      if (threadIdx.x == 0) p.st[v] = tent;
     }
   }
 }
 
-// ---------------------------------------------------------------- a3: Phase B + push
-template <int POL, bool PUSH, bool CW>
-__device__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, int32_t* Wout, Work& wk) {
-  const uint32_t cur = r % 3, nxt = (r + 1) % 3;
-  const uint32_t nT = ld_relaxed(&p.info->cnt[cur][0]);
-  const uint32_t nW = ld_relaxed(&p.info->cnt[cur][1]);
-  const uint32_t nC = ld_relaxed(&p.info->cnt[cur][2]);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nT + nW + nC;
-    if (CW) wk.v[W_B_VERT] += (unsigned long long)nT + nW + nC;
-  }
-  uint32_t* cnt_next = &p.info->cnt[nxt][0];
-
-  // thread bin: one vertex per lane; losers pushed with one atomic per warp
+// Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round.
+template <class S, bool CW>
+__device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, const int32_t* W, const uint32_t* nb,
+                                             Work& wk, uint32_t* s_win) {
+  S* st = (S*)p.st;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
   {
     const int32_t* Wb = W + bins.off[0];
-    int32_t* Ob = Wout + bins.off[0];
-    const uint32_t stride = gridDim.x * BLOCK;
-    for (uint32_t base = blockIdx.x * BLOCK + warp * 32; base < nT; base += stride) {
-      const uint32_t i = base + lane;
-      bool lose = false;
-      int32_t v = 0;
-      if (i < nT) {
-        v = Wb[i];
-        const uint32_t tent = color_of(p.st[v]);
-        const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
-        lose = conflict_thread<POL, CW>(p, v, tent, beg, end, wk);
-        if (!lose) {
-          p.st[v] = tent | COMMIT;
-          if (PUSH && tent <= 32) {
-            scatter_thread(p, 1u << (tent - 1), beg, end);
-            if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
-          }
-        }
-      }
-      const unsigned m = __ballot_sync(FULL, lose);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        uint32_t pos = 0;
-        if (lane == leader) pos = atomicAdd(&cnt_next[0], (uint32_t)__popc(m));
-        pos = __shfl_sync(FULL, pos, leader);
-        if (lose) Ob[pos + __popc(m & lanemask_lt())] = v;
-        if (CW && lane == leader) wk.v[W_PUSH] += __popc(m);
-      }
+    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nb[0]; i += gridDim.x * BLOCK) {
+      const int32_t v = ldw(Wb + i);
+      sts(st + v, firstfit_thread<S, CW>(p, v, 1u, wk));
     }
   }
-  // warp bin
+#pragma unroll
+  for (int b = 1; b <= 2; ++b) {
+    const int32_t* Wb = W + bins.off[b];
+    for (uint32_t i = gw; i < nb[b]; i += nw) {
+      const int32_t v = ldw(Wb + i);
+      const uint32_t t = firstfit_warp<S, CW>(p, v, 1u, wk, lane);
+      if (lane == 0) sts(st + v, t);
+    }
+  }
   {
-    const int32_t* Wb = W + bins.off[1];
-    int32_t* Ob = Wout + bins.off[1];
-    const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-    for (uint32_t i = gw; i < nW; i += nw) {
-      const int32_t v = Wb[i];
-      const uint32_t tent = color_of(p.st[v]);
+    const int32_t* Wb = W + bins.off[3];
+    for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
+      const int32_t v = ldw(Wb + i);
+      const uint32_t t = firstfit_cta<S, CW>(p, v, 1u, wk, s_win);
+      if (threadIdx.x == 0) sts(st + v, t);
+    }
+  }
+}
+
+template <class S, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, Work& wk) {
+  __shared__ uint32_t s_win[2];
+  const uint32_t cur = r % 3;
+  uint32_t nb[NBIN];
+#pragma unroll
+  for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
+  // reset the counters round r+1 will push into and the work queues it will pop from
+  // (last used in round r-2)
+  if (blockIdx.x == 0 && threadIdx.x < NBIN) {
+    p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
+    p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
+  }
+  if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1] + nb[2] + nb[3];
+  if (PUSH) phase_a_mask<S, CW>(p, bins, W, nb, wk);
+  else phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
+}
+
+// ---------------------------------------------------------------- a3: Phase B + push
+// Winners commit (set the top bit of their own word) and, in mask mode, OR their colour bit
+// into the forbidden mask of every neighbour; losers go to W_out through the Pusher.
+
+// bin 0: one vertex per lane
+// Warps pop chunks of CH items from a per-bin queue head (one atomic per chunk) so that
+// costly items (long scans) do not leave the rest of the grid idle at the phase barrier.
+template <uint32_t CH>
+__device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, int lane) {
+  uint32_t b = 0;
+  if (lane == 0) b = atomicAdd(q, (uint32_t)CH);
+  return __shfl_sync(FULL, b, 0);
+}
+
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_b_thread(const Params& p, const int32_t* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
+                                               Work& wk) {
+  S* st = (S*)p.st;
+  const int lane = threadIdx.x & 31;
+  constexpr uint32_t CH = 64;
+  for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
+    const uint32_t cend = min(c0 + CH, cnt);
+    for (uint32_t base = c0; base < cend; base += 32) {
+    const uint32_t i = base + lane;
+    bool lose = false;
+    int32_t v = 0;
+    if (i < cnt) {
+      v = ldw(Wb + i);
+      const uint32_t tent = lds(st + v) & SW<S>::CMASK;
       const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
-      const bool lose = conflict_warp<POL, CW>(p, v, tent, beg, end, wk, lane);
-      if (lose) {
-        if (lane == 0) {
-          Ob[atomicAdd(&cnt_next[1], 1u)] = v;
-          if (CW) wk.v[W_PUSH] += 1;
-        }
-      } else {
-        if (lane == 0) p.st[v] = tent | COMMIT;
+      lose = conflict_thread<S, POL, CW>(p, v, tent, beg, end, wk);
+      if (!lose) {
+        sts(st + v, tent | SW<S>::COMMIT);
         if (PUSH && tent <= 32) {
-          const uint32_t bit = 1u << (tent - 1);
-          for (int64_t e = beg + lane; e < end; e += 32) atomicOr(&p.fm[ldc(p.ci, e)], bit);
-          if (CW && lane == 0) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
+          scatter<1>(p, 1u << (tent - 1), beg, end);
+          if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
         }
       }
     }
+    pu.template push<0, CW>(lose, v, lane, wk.v[W_PUSH]);
   }
-  // CTA bin
+  }
+}
+
+// bins 1 and 2: one G-lane group per vertex (G = 8 or 32)
+template <class S, int G, int B, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_b_group(const Params& p, const int32_t* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
+                                              Work& wk) {
+  S* st = (S*)p.st;
+  constexpr int PER = 32 / G;
+  constexpr uint32_t CH = 8 * PER;
+  const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
+  for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
+  const uint32_t cend = min(c0 + CH, cnt);
+  for (uint32_t base = c0; base < cend; base += PER) {
+    const uint32_t i = base + grp;
+    const bool act = i < cnt;
+    int32_t v = 0;
+    uint32_t tent = 0;
+    int64_t beg = 0, end = 0;
+    if (act) {
+      v = ldw(Wb + i);
+      tent = lds(st + v) & SW<S>::CMASK;
+      beg = ldr(p.rp, v);
+      end = ldr(p.rp, v + 1);
+    }
+    const bool lose = conflict_group<S, G, POL, CW>(p, act, v, tent, beg, end, lane, wk);
+    if (act && !lose) {
+      if (gl == 0) sts(st + v, tent | SW<S>::COMMIT);
+      if (PUSH && tent <= 32) {
+        scatter<G>(p, 1u << (tent - 1), beg + gl, end);
+        if (CW && gl == 0) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
+      }
+    }
+    pu.template push<B, CW>(act && lose && gl == 0, v, lane, wk.v[W_PUSH]);
+  }
+  }
+}
+
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, int32_t* Wout,
+                                        Work& wk) {
+  __shared__ int32_t s_pbuf[WARPS][NBIN * PBUF];
+  __shared__ int s_first;
+  S* st = (S*)p.st;
+  const uint32_t cur = r % 3, nxt = (r + 1) % 3;
+  uint32_t nb[NBIN];
+#pragma unroll
+  for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1] + nb[2] + nb[3];
+    if (CW) wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1] + nb[2] + nb[3];
+  }
+  uint32_t* cnt_next = &p.info->cnt[nxt][0];
+  Pusher pu;
+  pu.init(s_pbuf[warp], Wout, cnt_next, bins);
+
+  phase_b_thread<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
+  phase_b_group<S, 8, 1, POL, PUSH, CW>(p, W + bins.off[1], nb[1], &p.info->qctr[cur][1][0], pu, wk);
+  phase_b_group<S, 32, 2, POL, PUSH, CW>(p, W + bins.off[2], nb[2], &p.info->qctr[cur][2][0], pu, wk);
+  pu.template flush<CW>(lane, wk.v[W_PUSH]);
+
+  // bin 3: one CTA per vertex (rare, huge degrees): direct push
   {
-    const int32_t* Wb = W + bins.off[2];
-    int32_t* Ob = Wout + bins.off[2];
-    for (uint32_t i = blockIdx.x; i < nC; i += gridDim.x) {
-      const int32_t v = Wb[i];
-      const uint32_t tent = color_of(p.st[v]);
+    const int32_t* Wb = W + bins.off[3];
+    int32_t* Ob = Wout + bins.off[3];
+    for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
+      const int32_t v = ldw(Wb + i);
+      const uint32_t tent = lds(st + v) & SW<S>::CMASK;
       const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
-      const bool lose = conflict_cta<POL, CW>(p, v, tent, beg, end, wk);
+      const bool lose = conflict_cta<S, POL, CW>(p, v, tent, beg, end, wk, &s_first);
       if (lose) {
         if (threadIdx.x == 0) {
-          Ob[atomicAdd(&cnt_next[2], 1u)] = v;
+          stw(Ob + atomicAdd(&cnt_next[3], 1u), v);
           if (CW) wk.v[W_PUSH] += 1;
         }
       } else {
-        if (threadIdx.x == 0) p.st[v] = tent | COMMIT;
+        if (threadIdx.x == 0) sts(st + v, tent | SW<S>::COMMIT);
         if (PUSH && tent <= 32) {
-          const uint32_t bit = 1u << (tent - 1);
-          for (int64_t e = beg + threadIdx.x; e < end; e += BLOCK) atomicOr(&p.fm[ldc(p.ci, e)], bit);
+          scatter<BLOCK>(p, 1u << (tent - 1), beg + threadIdx.x, end);
           if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
         }
       }
@@ -221,15 +290,18 @@ __device__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const int
 // |W_{r+1}| summed over bins (read after the barrier that ends Phase B of round r).
 __device__ __forceinline__ uint32_t next_total(const Params& p, uint32_t r) {
   const uint32_t nxt = (r + 1) % 3;
-  return ld_relaxed(&p.info->cnt[nxt][0]) + ld_relaxed(&p.info->cnt[nxt][1]) + ld_relaxed(&p.info->cnt[nxt][2]);
+  return ld_relaxed(&p.info->cnt[nxt][0]) + ld_relaxed(&p.info->cnt[nxt][1]) + ld_relaxed(&p.info->cnt[nxt][2]) +
+         ld_relaxed(&p.info->cnt[nxt][3]);
 }
 
 // ---------------------------------------------------------------- a5: finalize
-__device__ void epilogue(const Params& p) {
+template <class S>
+__device__ __forceinline__ void epilogue(const Params& p) {
+  const S* st = (const S*)p.st;
   uint32_t mx = 0;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < p.n; v += stride) {
-    const uint32_t c = color_of(p.st[v]);
+    const uint32_t c = lds(st + v) & SW<S>::CMASK;
     p.colors_out[v] = c;
     mx = c > mx ? c : mx;
   }
@@ -238,39 +310,43 @@ __device__ void epilogue(const Params& p) {
 }
 
 template <bool CW>
-__device__ void flush_work(const Params& p, Work& wk) {
-  if (!CW) return;
+__device__ __forceinline__ void flush_work(const Params& p, Work& wk) {
+  if constexpr (CW) {
 #pragma unroll
-  for (int k = 0; k < W_N; ++k) {
-    unsigned long long x = wk.v[k];
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&p.info->work[k], x);
+    for (int k = 0; k < W_N; ++k) {
+      unsigned long long x = wk.v[k];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+      if ((threadIdx.x & 31) == 0 && x) atomicAdd(&p.info->work[k], x);
+    }
   }
 }
 
 // ---------------------------------------------------------------- a4: persistent driver
 // One cooperative launch runs ingest, every round and finalize.  Per round: Phase A,
 // barrier, Phase B (+push), barrier; every CTA reads |W_{r+1}| and leaves together.
-template <int POL, bool PUSH, bool CW>
+template <class S, int POL, bool PUSH, bool CW>
 __global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
   Work wk;
   wk.zero();
-  prologue_count<PUSH>(p);
+  prologue_count<S, PUSH>(p);
   if (!grid_sync(p)) return;
   Bins bins;
   bins.load(p);
   prologue_scatter(p, bins);
   if (!grid_sync(p)) return;
 
-  int32_t* Win = p.wl0;
-  int32_t* Wout = p.wl1;
+  // The worklist pointers are re-read from DevInfo every round instead of being swapped in
+  // registers: with loop-carried pointer swaps, ptxas (12.9) was observed to reuse the
+  // uniform register holding one of them inside the grid barrier (truncated addresses).
   uint32_t r = 1;
   for (;;) {
+    int32_t* Win = (int32_t*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
+    int32_t* Wout = (int32_t*)ld_relaxed64(&p.info->wlp[r & 1]);
     if (r > 1) {
-      phase_a<PUSH, CW>(p, r, bins, Win, wk);
+      phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
       if (!grid_sync(p)) return;
     }
-    phase_b<POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
+    phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
     if (!grid_sync(p)) return;
     const uint32_t left = next_total(p, r);
     if (left == 0) break;
@@ -280,20 +356,17 @@ __global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
       return;
     }
     ++r;
-    int32_t* t = Win;
-    Win = Wout;
-    Wout = t;
   }
-  epilogue(p);
+  epilogue<S>(p);
   flush_work<CW>(p, wk);
   if (blockIdx.x == 0 && threadIdx.x == 0) p.info->rounds = r;
 }
 
 // ---------------------------------------------------------------- host-driven ablation
-// GC_FLAG_HOST_ROUNDS: the same phases, one (non-cooperative) launch each, the host
-// reading |W_{r+1}| after every round (the paper's "CPU ... controlling the progress").
+// GC_FLAG_HOST_ROUNDS: the same phases (32-bit state words), one non-cooperative launch
+// each, the host reading |W_{r+1}| after every round ("CPU ... controlling the progress").
 template <bool PUSH>
-__global__ void __launch_bounds__(BLOCK) k_prologue_count(Params p) { prologue_count<PUSH>(p); }
+__global__ void __launch_bounds__(BLOCK) k_prologue_count(Params p) { prologue_count<uint32_t, PUSH>(p); }
 __global__ void __launch_bounds__(BLOCK) k_prologue_scatter(Params p) {
   Bins b;
   b.load(p);
@@ -305,7 +378,7 @@ __global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, int32_t
   wk.zero();
   Bins b;
   b.load(p);
-  phase_a<PUSH, CW>(p, r, b, W, wk);
+  phase_a<uint32_t, PUSH, CW>(p, r, b, W, wk);
   flush_work<CW>(p, wk);
 }
 template <int POL, bool PUSH, bool CW>
@@ -314,12 +387,18 @@ __global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, int32_t
   wk.zero();
   Bins b;
   b.load(p);
-  phase_b<POL, PUSH, CW>(p, r, b, W, Wout, wk);
+  phase_b<uint32_t, POL, PUSH, CW>(p, r, b, W, Wout, wk);
   flush_work<CW>(p, wk);
 }
 __global__ void __launch_bounds__(BLOCK) k_epilogue(Params p, uint32_t r) {
-  epilogue(p);
+  epilogue<uint32_t>(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) p.info->rounds = r;
+}
+
+// Grid-barrier cost probe (diagnostics only: gc__bench_grid_sync).
+__global__ void __launch_bounds__(BLOCK) k_bench_sync(Params p, int iters) {
+  for (int i = 0; i < iters; ++i)
+    if (!grid_sync(p)) return;
 }
 
 // ---------------------------------------------------------------- validation (C9)
@@ -327,9 +406,11 @@ __global__ void __launch_bounds__(BLOCK) k_epilogue(Params p, uint32_t r) {
 // optionally symmetry by binary search of v in adj(w).  Records the smallest bad vertex.
 enum ValErr { VE_NONE = 0, VE_ROWPTR = 1, VE_RANGE = 2, VE_SELF = 3, VE_ORDER = 4, VE_ASYM = 5 };
 
+// I->bad starts at 0 (= nothing found); the smallest (vertex, code) key wins via atomicMax
+// of its complement, decoded on the host as ~bad.
 __device__ __forceinline__ void report_bad(DevInfo* I, int64_t v, uint32_t code) {
-  const unsigned long long key = ((unsigned long long)v << 3) | code;  // smallest vertex wins
-  atomicMin(&I->bad, key + 1);
+  const unsigned long long key = ((unsigned long long)v << 3) | code;
+  atomicMax(&I->bad, ~key);
 }
 
 __global__ void __launch_bounds__(BLOCK) k_validate(int32_t n, const int64_t* __restrict__ rp,
@@ -384,7 +465,7 @@ __global__ void __launch_bounds__(BLOCK) k_verify(int32_t n, const int64_t* __re
       lo = __reduce_or_sync(FULL, lo);
       hi = __reduce_or_sync(FULL, hi);
       // every colour in [base, min(c, base+64)) must be present
-      const uint32_t need = c - base;  // colours base..c-1
+      const uint32_t need = c - base;
       const unsigned long long have = ((unsigned long long)hi << 32) | lo;
       const unsigned long long want = need >= 64 ? ~0ull : ((1ull << need) - 1);
       if ((have & want) != want) bad = true;

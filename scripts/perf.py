@@ -1,0 +1,60 @@
+#!/usr/bin/env python
+"""Tuning sweeps on the GPU box (not part of the product or the bench contract).
+
+    python scripts/perf.py --config rmat24 --sweep bins
+Prints one line per variant: kernel ms (median of --reps), GTEPS, and whether the colours
+equal the default run's (they must: the result is schedule independent).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="rmat24")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sweep", default="default")
+    ap.add_argument("--barrier", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+    import paper_1606_06025_b200 as gc
+    import workloads as wl
+
+    if args.barrier:
+        for bps in (1, 2, 4, 0):
+            print(json.dumps({"barrier_us": gc.bench_grid_sync(0, bps, 2000), "blocks_per_sm": bps}), flush=True)
+
+    g = wl.config_graph(args.config)
+    rp = torch.from_numpy(g.row_ptr).cuda()
+    ci = torch.from_numpy(g.col_idx).cuda()
+    ref = gc.color(rp, ci, validate=False)
+    ref_c = ref.colors.clone()
+
+    variants = {"default": [dict()]}
+    variants["bins"] = [dict(thread_bin_max=t1, group_bin_max=t2, warp_bin_max=t3)
+                        for t1 in (8, 16, 24, 32) for t2 in (64, 128, 256) for t3 in (4096,)]
+    variants["grid"] = [dict(blocks_per_sm=b) for b in (1, 2, 3, 4, 5, 6, 8)]
+    variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
+                         dict(host_rounds=True, pull_firstfit=True)]
+    variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
+    for kw in variants[args.sweep]:
+        ts = []
+        res = None
+        for _ in range(args.reps):
+            res = gc.color(rp, ci, validate=False, time_kernel=True, **kw)
+            ts.append(res.kernel_ms)
+        ms = statistics.median(ts)
+        same = bool(torch.equal(res.colors, ref_c)) if "policy" not in kw else None
+        print(json.dumps({"config": args.config, "kw": kw, "kernel_ms": round(ms, 4),
+                          "gteps": round(g.m / ms / 1e6, 3), "rounds": res.rounds,
+                          "colors": res.num_colors, "same_as_default": same}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

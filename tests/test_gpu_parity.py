@@ -56,6 +56,7 @@ SMALL = [
     lambda: wl.gnp(300, 0.05, 1), lambda: wl.gnp(200, 0.3, 2), lambda: wl.rmat(12, 8),
     lambda: wl.rmat(12, 16, wl.GRAPH500, 3), lambda: wl.edgeless(1), lambda: wl.edgeless(1000),
     lambda: wl.disjoint_union(wl.complete(40), wl.path(7), wl.edgeless(3), wl.star(300)),
+    lambda: wl.star(40000), lambda: wl.disjoint_union(wl.rmat(10, 8), wl.star(33000, center_last=True)),
 ]
 
 
