@@ -157,15 +157,15 @@ void* pick_persistent(bool narrow, int pol, bool push, bool cw) {
 }
 
 template <int POL, bool PUSH, bool CW>
-void launch_phase_b(int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W, int32_t* Wo) {
+void launch_phase_b(int grid, cudaStream_t s, const Params& p, uint32_t r, WE* W, WE* Wo) {
   k_phase_b<POL, PUSH, CW><<<grid, BLOCK, 0, s>>>(p, r, W, Wo);
 }
 template <bool PUSH, bool CW>
-void launch_phase_a(int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W) {
+void launch_phase_a(int grid, cudaStream_t s, const Params& p, uint32_t r, WE* W) {
   k_phase_a<PUSH, CW><<<grid, BLOCK, 0, s>>>(p, r, W);
 }
 
-void launch_b(int pol, bool push, bool cw, int grid, cudaStream_t s, const Params& p, uint32_t r, int32_t* W, int32_t* Wo) {
+void launch_b(int pol, bool push, bool cw, int grid, cudaStream_t s, const Params& p, uint32_t r, WE* W, WE* Wo) {
 #define LB(P)                                                                   \
   if (pol == P) {                                                               \
     if (push) { if (cw) launch_phase_b<P, true, true>(grid, s, p, r, W, Wo); else launch_phase_b<P, true, false>(grid, s, p, r, W, Wo); } \
@@ -335,8 +335,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   void *st, *fm = nullptr, *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
   CK(sc.alloc(&st, sizeof(uint32_t) * (size_t)n));
   if (push) CK(sc.alloc(&fm, sizeof(uint32_t) * (size_t)n));
-  CK(sc.alloc(&w0, sizeof(int32_t) * (size_t)n));
-  CK(sc.alloc(&w1, sizeof(int32_t) * (size_t)n));
+  CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
+  CK(sc.alloc(&w1, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&info, sizeof(DevInfo)));
   CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
   if (!out_dev) CK(sc.alloc(&dcol, sizeof(uint32_t) * (size_t)n));
@@ -370,8 +370,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.ci = d_ci;
   p.st = (uint32_t*)st;
   p.fm = (uint32_t*)fm;
-  p.wl0 = (int32_t*)w0;
-  p.wl1 = (int32_t*)w1;
+  p.wl0 = (WE*)w0;
+  p.wl1 = (WE*)w1;
   p.info = (DevInfo*)info;
   p.trace = (uint32_t*)dtrace;
   p.trace_cap = trace ? o.trace_capacity : 0;
@@ -445,8 +445,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     else k_prologue_count<false><<<grid, BLOCK, 0, s>>>(p);
     k_prologue_scatter<<<grid, BLOCK, 0, s>>>(p);
     CK(cudaGetLastError());
-    int32_t* W = p.wl0;
-    int32_t* Wo = p.wl1;
+    WE* W = p.wl0;
+    WE* Wo = p.wl1;
     uint32_t r = 1;
     uint32_t cnt[3][NBIN];
     for (;;) {
@@ -454,10 +454,36 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
         if (push) { if (cw) launch_phase_a<true, true>(grid, s, p, r, W); else launch_phase_a<true, false>(grid, s, p, r, W); }
         else { if (cw) launch_phase_a<false, true>(grid, s, p, r, W); else launch_phase_a<false, false>(grid, s, p, r, W); }
       }
+#ifdef GC_HOSTDBG
+      { cudaError_t e = cudaStreamSynchronize(s); fprintf(stderr, "HOSTDBG r=%u after A: %s\n", r, cudaGetErrorName(e)); }
+#endif
       launch_b((int)o.policy, push, cw, grid, s, p, r, W, Wo);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(cnt, ((DevInfo*)info)->cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+#ifdef GC_HOSTDBG
+      {
+        const uint32_t* nx = cnt[(r + 1) % 3];
+        uint32_t bs[NBIN];
+        cudaMemcpy(bs, ((DevInfo*)info)->binsize, sizeof(bs), cudaMemcpyDeviceToHost);
+        uint32_t off = 0;
+        for (int b = 0; b < NBIN; ++b) {
+          if (nx[b] > bs[b]) fprintf(stderr, "HOSTDBG r=%u bin %d count %u > cap %u\n", r, b, nx[b], bs[b]);
+          WE* h = (WE*)malloc(sizeof(WE) * (nx[b] + 1));
+          cudaMemcpy(h, Wo + off, sizeof(WE) * nx[b], cudaMemcpyDeviceToHost);
+          for (uint32_t i = 0; i < nx[b]; ++i) {
+            int64_t rb = 0;
+            if (h[i].v < 0 || h[i].v >= n) { fprintf(stderr, "HOSTDBG r=%u bin %d i %u bad v %d\n", r, b, i, h[i].v); break; }
+            cudaMemcpy(&rb, d_rp + h[i].v, 8, cudaMemcpyDeviceToHost);
+            if (rb != h[i].beg || h[i].k < 0) { fprintf(stderr, "HOSTDBG r=%u bin %d i %u v %d k %d beg %lld rp %lld\n", r, b, i, h[i].v, h[i].k, h[i].beg, (long long)rb); break; }
+            if (i > 64) break;
+          }
+          free(h);
+          off += bs[b];
+        }
+        fprintf(stderr, "HOSTDBG r=%u after B: next=%u %u %u %u\n", r, nx[0], nx[1], nx[2], nx[3]);
+      }
+#endif
       const uint32_t* nx = cnt[(r + 1) % 3];
       if (nx[0] + nx[1] + nx[2] + nx[3] == 0) break;
       if (r >= p.max_rounds) {
@@ -465,7 +491,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
         return GC_ERR_NO_CONVERGENCE;
       }
       ++r;
-      int32_t* t = W;
+      WE* t = W;
       W = Wo;
       Wo = t;
     }

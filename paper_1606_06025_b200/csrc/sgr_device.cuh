@@ -26,11 +26,12 @@
 //     per directed edge over the whole run) and Phase A is O(1): tent = ffs(~fm[v]); only a
 //     full mask falls back to the exact windowed scan from colour 33 (reading C7).
 //     GC_FLAG_PULL_FIRSTFIT selects the paper's full rescan instead (same result).
-//   * L2 eviction priorities: the per-vertex state (st, fm) is loaded/stored evict_last,
-//     the streamed CSR and worklists evict_first.
+//   * L1 policy: the read-only CSR goes through the non-coherent path without allocating
+//     in L1; everything written during the run is read L2-coherently (.cg).
 //   * Round 1 needs no Phase A: nothing is committed, so every tentative colour is 1.
 #pragma once
 #include <cuda_runtime.h>
+
 #include <stdint.h>
 
 namespace gcdev {
@@ -77,14 +78,23 @@ struct DevInfo {
   uint32_t pad4[31];
 };
 
+// Worklist entry: the vertex, the split k = number of its neighbours with a lower id
+// (-1 = not yet known; rows are sorted so adj(v) = [beg, beg+k) lower ids, [beg+k, end) higher
+// ids) and its row start, so that Phase B can start the conflict scan without reading row_ptr.
+struct __align__(16) WE {
+  int32_t v;
+  int32_t k;
+  long long beg;
+};
+
 struct Params {
   int32_t n;
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;
   void* st;                     // state word per vertex (uint16_t or uint32_t)
   uint32_t* fm;                 // forbidden colours 1..32 per vertex (incremental mode)
-  int32_t* wl0;                 // worklist buffers, n entries each, bin segments
-  int32_t* wl1;
+  WE* wl0;                      // worklist buffers, n entries each, bin segments
+  WE* wl1;
   DevInfo* info;
   uint32_t* trace;
   uint32_t trace_cap;
@@ -105,58 +115,71 @@ struct Work {
 };
 
 // ---------------------------------------------------------------- memory helpers
-// L2 eviction-priority policies (createpolicy, sm_80+).
-__device__ __forceinline__ uint64_t pol_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 
-// CSR: read-only for the whole kernel (non-coherent path), streamed (evict_first).
+// Memory access helpers.  Only L1-level hints are used: the L2 cache_hint forms
+// (createpolicy + ld/st/red .L2::cache_hint) were observed to make ptxas 12.9 (sm_100a)
+// emit code that clobbers live uniform registers in this kernel.
+// CSR: read-only for the whole kernel -> non-coherent path, not allocated in L1 (streamed).
 __device__ __forceinline__ int32_t ldc(const int32_t* __restrict__ p, int64_t i) {
   int32_t v;
-  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p + i), "l"(pol_first()));
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p + i));
   return v;
 }
 __device__ __forceinline__ int64_t ldr(const int64_t* __restrict__ p, int64_t i) {
   int64_t v;
-  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p + i), "l"(pol_first()));
+  asm("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p + i));
   return v;
 }
-// Worklists: written in one phase, read after a barrier (coherent loads), streamed.
-__device__ __forceinline__ int32_t ldw(const int32_t* p) {
+// Everything written inside the run (worklists, state words, forbidden masks) is read with
+// ld.global.cg (L2 only, never L1): with L1-cacheable weak loads of the state words the
+// host-driven ablation (one launch per phase) was observed to read stale lines across
+// kernel boundaries on this B200/driver; .cg costs nothing measurable.
+// Worklists: written in one phase, read after a barrier, streamed.
+__device__ __forceinline__ WE ldw(const WE* p) {
+  WE e;
+  uint32_t lo, hi;
+  asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(e.v), "=r"(e.k), "=r"(lo), "=r"(hi)
+               : "l"(p)
+               : "memory");
+  e.beg = (long long)(((unsigned long long)hi << 32) | lo);
+  return e;
+}
+__device__ __forceinline__ int32_t ldw_v(const WE* p) {
   int32_t v;
-  asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_first()) : "memory");
+  asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(&p->v) : "memory");
   return v;
 }
-__device__ __forceinline__ void stw(int32_t* p, int32_t v) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol_first()) : "memory");
+__device__ __forceinline__ void stw(WE* p, const WE& e) {
+  const unsigned long long b = (unsigned long long)e.beg;
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(e.v), "r"(e.k), "r"((uint32_t)b),
+               "r"((uint32_t)(b >> 32))
+               : "memory");
 }
-// Per-vertex state: kept resident (evict_last).
+// Per-vertex state words and forbidden masks (L2-resident working set).
 __device__ __forceinline__ uint32_t lds(const uint16_t* p) {
   uint16_t v;
-  asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol_last()) : "memory");
+  asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t lds(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_last()) : "memory");
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void sts(uint16_t* p, uint32_t v) {
-  asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(p), "h"((uint16_t)v), "l"(pol_last()) : "memory");
+  asm volatile("st.global.u16 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
 }
 __device__ __forceinline__ void sts(uint32_t* p, uint32_t v) {
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol_last()) : "memory");
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ldf(const uint32_t* p) { return lds(p); }
+__device__ __forceinline__ uint32_t ldf(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t bit) {
-  asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(bit), "l"(pol_last()) : "memory");
+  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(p), "r"(bit) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
@@ -242,12 +265,12 @@ struct Bins {
 // with ONE global atomic per 32 pushes (coalesced 128-B stores); remainders are flushed at
 // the end of the phase.  Counts are warp-uniform registers.
 struct Pusher {
-  int32_t* buf;            // this warp's [NBIN][PBUF] staging area (shared memory)
-  int32_t* out;            // W_out
+  WE* buf;                 // this warp's [NBIN][PBUF] staging area (shared memory)
+  WE* out;                 // W_out
   uint32_t* gcnt;          // &info->cnt[next][0]
   uint32_t off[NBIN];
   uint32_t c[NBIN];
-  __device__ __forceinline__ void init(int32_t* b, int32_t* o, uint32_t* g, const Bins& bins) {
+  __device__ __forceinline__ void init(WE* b, WE* o, uint32_t* g, const Bins& bins) {
     buf = b;
     out = o;
     gcnt = g;
@@ -255,10 +278,10 @@ struct Pusher {
     for (int k = 0; k < NBIN; ++k) { off[k] = bins.off[k]; c[k] = 0; }
   }
   template <int B, bool CW>
-  __device__ __forceinline__ void push(bool pred, int32_t v, int lane, unsigned long long& pushed) {
+  __device__ __forceinline__ void push(bool pred, const WE& v, int lane, unsigned long long& pushed) {
     const unsigned m = __ballot_sync(FULL, pred);
     if (!m) return;
-    int32_t* bb = buf + B * PBUF;
+    WE* bb = buf + B * PBUF;
     if (pred) bb[c[B] + __popc(m & lanemask_lt())] = v;
     c[B] += __popc(m);
     if (c[B] >= 32) {
@@ -268,7 +291,8 @@ struct Pusher {
       pos = __shfl_sync(FULL, pos, 0);
       stw(out + off[B] + pos + lane, bb[lane]);
       const uint32_t rest = c[B] - 32;
-      const int32_t x = (uint32_t)lane < rest ? bb[32 + lane] : 0;
+      WE x;
+      if ((uint32_t)lane < rest) x = bb[32 + lane];
       __syncwarp();
       if ((uint32_t)lane < rest) bb[lane] = x;
       __syncwarp();
@@ -396,138 +420,139 @@ __device__ __forceinline__ bool recolors(const Params& p, int32_t v, int32_t w, 
 }
 
 // ---------------------------------------------------------------- Phase B scans
-// Each returns true when v must recolour (is pushed to W_out).  HIGHER_ID only needs the
-// lower-id prefix of the (sorted) row and stops at the first w > v or the first hit;
-// LOWER_ID scans the upper suffix from the end; DEGREE scans the whole row.  Work counters
-// (CW) follow the sequential scan, whatever the lane mapping.
+// v must recolour iff some neighbour w in the policy's scan range has the same tentative
+// colour (and, for DEGREE, priority over v).  Because rows are sorted, the range is contiguous:
+//   HIGHER_ID: the lower ids [beg, beg+k), scanned from the top down — nearest lower ids first:
+//              pending vertices are biased to high ids, so conflicts are found ~2.4x sooner on
+//              R-MAT than with an ascending scan (same predicate, different order: exact);
+//   LOWER_ID : the higher ids [beg+k, end), scanned upwards from the split;
+//   DEGREE   : the whole row.
+// Work counters (CW) follow the sequential scan in that order, whatever the lane mapping.
 
-template <class S, int POL, bool CW>
-__device__ __forceinline__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end,
-                                                Work& wk) {
-  const S* st = (const S*)p.st;
-  constexpr uint32_t CM = SW<S>::CMASK;
-  if (POL == HIGHER_ID) {
-    int64_t e = beg;
-    for (; e + 4 <= end; e += 4) {
-      const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + 1), w2 = ldc(p.ci, e + 2), w3 = ldc(p.ci, e + 3);
-      // speculative gathers of the lower-id candidates (rows are sorted: w0<w1<w2<w3)
-      const uint32_t c0 = w0 < v ? (lds(st + w0) & CM) : 0u;
-      const uint32_t c1 = w1 < v ? (lds(st + w1) & CM) : 0u;
-      const uint32_t c2 = w2 < v ? (lds(st + w2) & CM) : 0u;
-      const uint32_t c3 = w3 < v ? (lds(st + w3) & CM) : 0u;
-      if (w0 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 1; wk.v[W_B_GATHER] += e - beg; } return false; }
-      if (c0 == tent) { if (CW) { wk.v[W_B_EDGE] += e - beg + 1; wk.v[W_B_GATHER] += e - beg + 1; } return true; }
-      if (w1 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 2; wk.v[W_B_GATHER] += e - beg + 1; } return false; }
-      if (c1 == tent) { if (CW) { wk.v[W_B_EDGE] += e - beg + 2; wk.v[W_B_GATHER] += e - beg + 2; } return true; }
-      if (w2 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 3; wk.v[W_B_GATHER] += e - beg + 2; } return false; }
-      if (c2 == tent) { if (CW) { wk.v[W_B_EDGE] += e - beg + 3; wk.v[W_B_GATHER] += e - beg + 3; } return true; }
-      if (w3 > v) { if (CW) { wk.v[W_B_EDGE] += e - beg + 4; wk.v[W_B_GATHER] += e - beg + 3; } return false; }
-      if (c3 == tent) { if (CW) { wk.v[W_B_EDGE] += e - beg + 4; wk.v[W_B_GATHER] += e - beg + 4; } return true; }
-    }
-    for (; e < end; ++e) {
-      const int32_t w = ldc(p.ci, e);
-      if (CW) wk.v[W_B_EDGE] += 1;
-      if (w > v) return false;
-      if (CW) wk.v[W_B_GATHER] += 1;
-      if ((lds(st + w) & CM) == tent) return true;
-    }
-    return false;
-  } else if (POL == LOWER_ID) {
-    for (int64_t e = end - 1; e >= beg; --e) {
-      const int32_t w = ldc(p.ci, e);
-      if (CW) wk.v[W_B_EDGE] += 1;
-      if (w < v) return false;
-      if (CW) wk.v[W_B_GATHER] += 1;
-      if ((lds(st + w) & CM) == tent) return true;
-    }
-    return false;
-  } else {
-    const int64_t dv = end - beg;
-    for (int64_t e = beg; e < end; ++e) {
-      const int32_t w = ldc(p.ci, e);
-      if (CW) { wk.v[W_B_EDGE] += 1; wk.v[W_B_GATHER] += 1; }
-      if ((lds(st + w) & CM) == tent && recolors<DEGREE>(p, v, w, dv)) return true;
-    }
-    return false;
-  }
+template <int POL>
+struct ScanRange {
+  int64_t lo, hi;   // [lo, hi) of row positions
+  bool down;        // scan from hi-1 downwards
+};
+template <int POL>
+__device__ __forceinline__ ScanRange<POL> scan_range(int64_t beg, int32_t k, int64_t end) {
+  if (POL == HIGHER_ID) return {beg, beg + k, true};
+  if (POL == LOWER_ID) return {beg + k, end, false};
+  return {beg, end, false};
 }
 
-// Group scan: a group of G lanes (G = 8 or 32, aligned in the warp) examines its vertex's row
-// G entries per step.  Called by the whole warp in lockstep (warp-uniform loop); inactive
+// Split of v's sorted row [beg, end): number of neighbours with id < v (binary search).
+__device__ __forceinline__ int32_t row_split(const Params& p, int32_t v, int64_t beg, int64_t end) {
+  int64_t lo = beg, hi = end;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ldc(p.ci, mid) < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return (int32_t)(lo - beg);
+}
+
+template <class S, int POL, bool CW>
+__device__ __forceinline__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64_t lo, int64_t hi,
+                                                bool down, int64_t dv, Work& wk) {
+  const S* st = (const S*)p.st;
+  constexpr uint32_t CM = SW<S>::CMASK;
+  const int64_t len = hi - lo;
+  int64_t j = 0;
+  for (; j + 4 <= len; j += 4) {
+    const int64_t e = down ? hi - 1 - j : lo + j;
+    const int64_t d = down ? -1 : 1;
+    const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + d), w2 = ldc(p.ci, e + 2 * d), w3 = ldc(p.ci, e + 3 * d);
+    const uint32_t c0 = lds(st + w0) & CM, c1 = lds(st + w1) & CM, c2 = lds(st + w2) & CM, c3 = lds(st + w3) & CM;
+    const bool h0 = c0 == tent && recolors<POL>(p, v, w0, dv);
+    const bool h1 = c1 == tent && recolors<POL>(p, v, w1, dv);
+    const bool h2 = c2 == tent && recolors<POL>(p, v, w2, dv);
+    const bool h3 = c3 == tent && recolors<POL>(p, v, w3, dv);
+    if (h0 | h1 | h2 | h3) {
+      if (CW) {
+        const int f = h0 ? 1 : h1 ? 2 : h2 ? 3 : 4;
+        wk.v[W_B_EDGE] += j + f;
+        wk.v[W_B_GATHER] += j + f;
+      }
+      return true;
+    }
+  }
+  for (; j < len; ++j) {
+    const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
+    if ((lds(st + w) & CM) == tent && recolors<POL>(p, v, w, dv)) {
+      if (CW) { wk.v[W_B_EDGE] += j + 1; wk.v[W_B_GATHER] += j + 1; }
+      return true;
+    }
+  }
+  if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
+  return false;
+}
+
+// Group scan: a group of G lanes (G = 8 or 32, aligned in the warp) examines G positions of
+// its range per step.  Called by the whole warp in lockstep (warp-uniform loop); inactive
 // groups pass act = false.  Returns the group's verdict in every lane of the group.
 template <class S, int G, int POL, bool CW>
-__device__ __forceinline__ bool conflict_group(const Params& p, bool act, int32_t v, uint32_t tent, int64_t beg,
-                                               int64_t end, int lane, Work& wk) {
+__device__ __forceinline__ bool conflict_group(const Params& p, bool act, int32_t v, uint32_t tent, int64_t lo,
+                                               int64_t hi, bool down, int64_t dv, int lane, Work& wk) {
   const S* st = (const S*)p.st;
   const int gl = lane % G;
   const int shift = (lane / G) * G;
   const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << shift);
-  const int64_t len = act ? end - beg : 0;
-  const int64_t dv = end - beg;
-  bool done = len == 0;
+  const int64_t len = act ? hi - lo : 0;
+  bool done = len <= 0;
   bool lose = false;
   for (int64_t k = 0;; k += G) {
     if (__all_sync(FULL, done)) break;
-    bool hit = false, stop = false, side = false, valid = false;
+    bool hit = false, valid = false;
     if (!done) {
       const int64_t j = k + gl;
       valid = j < len;
-      const int64_t e = (POL == LOWER_ID) ? end - 1 - j : beg + j;
-      const int32_t w = valid ? ldc(p.ci, e) : v;
-      if (POL == HIGHER_ID) side = valid && w < v;
-      else if (POL == LOWER_ID) side = valid && w > v;
-      else side = valid;
-      if (side) hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
-      stop = hit || !side;
+      if (valid) {
+        const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
+        hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
+      }
     }
     const unsigned hb = __ballot_sync(FULL, hit) & gmask;
-    const unsigned sb = __ballot_sync(FULL, stop) & gmask;
     if (CW) {
       const unsigned vb = __ballot_sync(FULL, valid) & gmask;
-      const unsigned db = __ballot_sync(FULL, side) & gmask;
       if (!done && gl == 0) {
-        const int f = sb ? __ffs(sb >> shift) - 1 : G - 1;  // the sequential scan stops here
+        const int f = hb ? __ffs(hb >> shift) - 1 : G - 1;  // the sequential scan stops here
         const unsigned upto = (f >= 31 ? FULL : ((2u << f) - 1u)) << shift;
         wk.v[W_B_EDGE] += __popc(vb & upto);
-        wk.v[W_B_GATHER] += __popc(db & upto);
+        wk.v[W_B_GATHER] += __popc(vb & upto);
       }
     }
     if (!done) {
       if (hb) { lose = true; done = true; }
-      else if (sb || k + G >= len) done = true;
+      else if (k + G >= len) done = true;
     }
   }
   return lose;
 }
 
 template <class S, int POL, bool CW>
-__device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t beg, int64_t end,
-                                             Work& wk, int* s_first) {
+__device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_t tent, int64_t lo, int64_t hi,
+                                             bool down, int64_t dv, Work& wk, int* s_first) {
   const S* st = (const S*)p.st;
-  const int64_t dv = end - beg;
-  const int64_t len = end - beg;
+  const int64_t len = hi - lo;
   for (int64_t k = 0; k < len; k += BLOCK) {
     const int64_t j = k + threadIdx.x;
     const bool valid = j < len;
-    const int64_t e = (POL == LOWER_ID) ? end - 1 - j : beg + j;
-    const int32_t w = valid ? ldc(p.ci, e) : v;
-    bool side, hit = false;
-    if (POL == HIGHER_ID) side = valid && w < v;
-    else if (POL == LOWER_ID) side = valid && w > v;
-    else side = valid;
-    if (side) hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
+    bool hit = false;
+    if (valid) {
+      const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
+      hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
+    }
     if (CW) {
       if (threadIdx.x == 0) *s_first = BLOCK;
       __syncthreads();
-      if (hit || !side) atomicMin(s_first, (int)threadIdx.x);
+      if (hit) atomicMin(s_first, (int)threadIdx.x);
       __syncthreads();
       const int kk = *s_first < BLOCK ? *s_first : BLOCK - 1;
       const int ne = __syncthreads_count(valid && (int)threadIdx.x <= kk);
-      const int ng = __syncthreads_count(side && (int)threadIdx.x <= kk);
-      if (threadIdx.x == 0) { wk.v[W_B_EDGE] += ne; wk.v[W_B_GATHER] += ng; }
+      if (threadIdx.x == 0) { wk.v[W_B_EDGE] += ne; wk.v[W_B_GATHER] += ne; }
     }
     if (__syncthreads_or(hit)) return true;
-    if (__syncthreads_or(!side)) return false;
   }
   return false;
 }

@@ -55,7 +55,14 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
   for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
-    const int b = act ? bin_of(p, ldr(p.rp, v + 1) - ldr(p.rp, v)) : -1;
+    int b = -1;
+    WE e;
+    if (act) {
+      e.v = (int32_t)v;
+      e.k = -1;  // split computed by the first Phase B visit
+      e.beg = ldr(p.rp, v);
+      b = bin_of(p, ldr(p.rp, v + 1) - e.beg);
+    }
 #pragma unroll
     for (int k = 0; k < NBIN; ++k) {
       const unsigned m = __ballot_sync(FULL, b == k);
@@ -64,7 +71,7 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
       uint32_t pos = 0;
       if (lane == leader) pos = atomicAdd(&p.info->cursor[k], (uint32_t)__popc(m));
       pos = __shfl_sync(FULL, pos, leader);
-      if (b == k) stw(p.wl0 + bins.off[k] + pos + __popc(m & lanemask_lt()), (int32_t)v);
+      if (b == k) stw(p.wl0 + bins.off[k] + pos + __popc(m & lanemask_lt()), e);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = p.info->binsize[threadIdx.x];
@@ -75,14 +82,14 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
 // processed thread-per-vertex; a vertex whose 32-colour mask is full is handed to the whole
 // warp, which runs the exact windowed First-Fit from colour 33 (reading C7).
 template <class S, bool CW>
-__device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, const int32_t* W, const uint32_t* nb,
+__device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, const WE* W, const uint32_t* nb,
                                              Work& wk) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) {
-    const int32_t* Wb = W + bins.off[b];
+    const WE* Wb = W + bins.off[b];
     const uint32_t cnt = nb[b];
     for (uint32_t base = gw * 32; base < cnt; base += nw * 32) {
       const uint32_t i = base + lane;
@@ -90,7 +97,7 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, 
       int32_t v = 0;
       uint32_t f = 0;
       if (act) {
-        v = ldw(Wb + i);
+        v = ldw_v(Wb + i);
         f = ldf(p.fm + v);
       }
       const bool fb = act && f == FULL;
@@ -109,31 +116,31 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, 
 
 // Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round.
 template <class S, bool CW>
-__device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, const int32_t* W, const uint32_t* nb,
+__device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, const WE* W, const uint32_t* nb,
                                              Work& wk, uint32_t* s_win) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
   {
-    const int32_t* Wb = W + bins.off[0];
+    const WE* Wb = W + bins.off[0];
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nb[0]; i += gridDim.x * BLOCK) {
-      const int32_t v = ldw(Wb + i);
+      const int32_t v = ldw_v(Wb + i);
       sts(st + v, firstfit_thread<S, CW>(p, v, 1u, wk));
     }
   }
 #pragma unroll
   for (int b = 1; b <= 2; ++b) {
-    const int32_t* Wb = W + bins.off[b];
+    const WE* Wb = W + bins.off[b];
     for (uint32_t i = gw; i < nb[b]; i += nw) {
-      const int32_t v = ldw(Wb + i);
+      const int32_t v = ldw_v(Wb + i);
       const uint32_t t = firstfit_warp<S, CW>(p, v, 1u, wk, lane);
       if (lane == 0) sts(st + v, t);
     }
   }
   {
-    const int32_t* Wb = W + bins.off[3];
+    const WE* Wb = W + bins.off[3];
     for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
-      const int32_t v = ldw(Wb + i);
+      const int32_t v = ldw_v(Wb + i);
       const uint32_t t = firstfit_cta<S, CW>(p, v, 1u, wk, s_win);
       if (threadIdx.x == 0) sts(st + v, t);
     }
@@ -141,7 +148,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
 }
 
 template <class S, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, Work& wk) {
+__device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const WE* W, Work& wk) {
   __shared__ uint32_t s_win[2];
   const uint32_t cur = r % 3;
   uint32_t nb[NBIN];
@@ -173,7 +180,7 @@ __device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, int lane) {
 }
 
 template <class S, int POL, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_b_thread(const Params& p, const int32_t* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
+__device__ __forceinline__ void phase_b_thread(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
                                                Work& wk) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
@@ -181,67 +188,82 @@ __device__ __forceinline__ void phase_b_thread(const Params& p, const int32_t* W
   for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
     const uint32_t cend = min(c0 + CH, cnt);
     for (uint32_t base = c0; base < cend; base += 32) {
-    const uint32_t i = base + lane;
-    bool lose = false;
-    int32_t v = 0;
-    if (i < cnt) {
-      v = ldw(Wb + i);
-      const uint32_t tent = lds(st + v) & SW<S>::CMASK;
-      const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
-      lose = conflict_thread<S, POL, CW>(p, v, tent, beg, end, wk);
-      if (!lose) {
-        sts(st + v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 32) {
-          scatter<1>(p, 1u << (tent - 1), beg, end);
-          if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
+      const uint32_t i = base + lane;
+      bool lose = false;
+      WE e;
+      if (i < cnt) {
+        e = ldw(Wb + i);
+        const int32_t v = e.v;
+        const uint32_t tent = lds(st + v) & SW<S>::CMASK;
+        // the row end is needed for the split (first visit), the upper range and the scatter
+        int64_t end = -1;
+        if (e.k < 0 || POL != HIGHER_ID) end = ldr(p.rp, v + 1);
+        if (e.k < 0 && POL != DEGREE) e.k = row_split(p, v, e.beg, end);
+        const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+        lose = conflict_thread<S, POL, CW>(p, v, tent, sr.lo, sr.hi, sr.down, POL == DEGREE ? end - e.beg : 0, wk);
+        if (!lose) {
+          sts(st + v, tent | SW<S>::COMMIT);
+          if (PUSH && tent <= 32) {
+            if (end < 0) end = ldr(p.rp, v + 1);
+            scatter<1>(p, 1u << (tent - 1), e.beg, end);
+            if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+          }
         }
       }
+      pu.template push<0, CW>(lose, e, lane, wk.v[W_PUSH]);
     }
-    pu.template push<0, CW>(lose, v, lane, wk.v[W_PUSH]);
-  }
   }
 }
 
 // bins 1 and 2: one G-lane group per vertex (G = 8 or 32)
 template <class S, int G, int B, int POL, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_b_group(const Params& p, const int32_t* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
+__device__ __forceinline__ void phase_b_group(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
                                               Work& wk) {
   S* st = (S*)p.st;
   constexpr int PER = 32 / G;
   constexpr uint32_t CH = 8 * PER;
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
+  const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << (grp * G));
   for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
-  const uint32_t cend = min(c0 + CH, cnt);
-  for (uint32_t base = c0; base < cend; base += PER) {
-    const uint32_t i = base + grp;
-    const bool act = i < cnt;
-    int32_t v = 0;
-    uint32_t tent = 0;
-    int64_t beg = 0, end = 0;
-    if (act) {
-      v = ldw(Wb + i);
-      tent = lds(st + v) & SW<S>::CMASK;
-      beg = ldr(p.rp, v);
-      end = ldr(p.rp, v + 1);
-    }
-    const bool lose = conflict_group<S, G, POL, CW>(p, act, v, tent, beg, end, lane, wk);
-    if (act && !lose) {
-      if (gl == 0) sts(st + v, tent | SW<S>::COMMIT);
-      if (PUSH && tent <= 32) {
-        scatter<G>(p, 1u << (tent - 1), beg + gl, end);
-        if (CW && gl == 0) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
+    const uint32_t cend = min(c0 + CH, cnt);
+    for (uint32_t base = c0; base < cend; base += PER) {
+      const uint32_t i = base + grp;
+      const bool act = i < cnt;
+      WE e;
+      e.v = 0;
+      e.k = 0;
+      e.beg = 0;
+      uint32_t tent = 0;
+      int64_t end = 0;
+      if (act) {
+        e = ldw(Wb + i);
+        tent = lds(st + e.v) & SW<S>::CMASK;
+        end = ldr(p.rp, e.v + 1);
+        // first visit: the group leader finds the split, then shares it
+        if (e.k < 0 && POL != DEGREE && gl == 0) e.k = row_split(p, e.v, e.beg, end);
       }
+      e.k = __shfl_sync(FULL, e.k, lane & ~(G - 1));
+      (void)gmask;
+      const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+      const bool lose = conflict_group<S, G, POL, CW>(p, act, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, lane, wk);
+      if (act && !lose) {
+        if (gl == 0) sts(st + e.v, tent | SW<S>::COMMIT);
+        if (PUSH && tent <= 32) {
+          scatter<G>(p, 1u << (tent - 1), e.beg + gl, end);
+          if (CW && gl == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+        }
+      }
+      pu.template push<B, CW>(act && lose && gl == 0, e, lane, wk.v[W_PUSH]);
     }
-    pu.template push<B, CW>(act && lose && gl == 0, v, lane, wk.v[W_PUSH]);
-  }
   }
 }
 
 template <class S, int POL, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const int32_t* W, int32_t* Wout,
+__device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const WE* W, WE* Wout,
                                         Work& wk) {
-  __shared__ int32_t s_pbuf[WARPS][NBIN * PBUF];
+  __shared__ WE s_pbuf[WARPS][NBIN * PBUF];
   __shared__ int s_first;
+  __shared__ int32_t s_k;
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   uint32_t nb[NBIN];
@@ -263,23 +285,30 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
 
   // bin 3: one CTA per vertex (rare, huge degrees): direct push
   {
-    const int32_t* Wb = W + bins.off[3];
-    int32_t* Ob = Wout + bins.off[3];
+    const WE* Wb = W + bins.off[3];
+    WE* Ob = Wout + bins.off[3];
     for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
-      const int32_t v = ldw(Wb + i);
-      const uint32_t tent = lds(st + v) & SW<S>::CMASK;
-      const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
-      const bool lose = conflict_cta<S, POL, CW>(p, v, tent, beg, end, wk, &s_first);
+      WE e = ldw(Wb + i);
+      const uint32_t tent = lds(st + e.v) & SW<S>::CMASK;
+      const int64_t end = ldr(p.rp, e.v + 1);
+      if (e.k < 0 && POL != DEGREE) {
+        if (threadIdx.x == 0) s_k = row_split(p, e.v, e.beg, end);
+        __syncthreads();
+        e.k = s_k;
+        __syncthreads();
+      }
+      const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+      const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, &s_first);
       if (lose) {
         if (threadIdx.x == 0) {
-          stw(Ob + atomicAdd(&cnt_next[3], 1u), v);
+          stw(Ob + atomicAdd(&cnt_next[3], 1u), e);
           if (CW) wk.v[W_PUSH] += 1;
         }
       } else {
-        if (threadIdx.x == 0) sts(st + v, tent | SW<S>::COMMIT);
+        if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
         if (PUSH && tent <= 32) {
-          scatter<BLOCK>(p, 1u << (tent - 1), beg + threadIdx.x, end);
-          if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - beg);
+          scatter<BLOCK>(p, 1u << (tent - 1), e.beg + threadIdx.x, end);
+          if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
         }
       }
       __syncthreads();
@@ -340,8 +369,8 @@ __global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
   // uniform register holding one of them inside the grid barrier (truncated addresses).
   uint32_t r = 1;
   for (;;) {
-    int32_t* Win = (int32_t*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
-    int32_t* Wout = (int32_t*)ld_relaxed64(&p.info->wlp[r & 1]);
+    WE* Win = (WE*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
+    WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
     if (r > 1) {
       phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
       if (!grid_sync(p)) return;
@@ -373,7 +402,7 @@ __global__ void __launch_bounds__(BLOCK) k_prologue_scatter(Params p) {
   prologue_scatter(p, b);
 }
 template <bool PUSH, bool CW>
-__global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, int32_t* W) {
+__global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, WE* W) {
   Work wk;
   wk.zero();
   Bins b;
@@ -382,7 +411,7 @@ __global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, int32_t
   flush_work<CW>(p, wk);
 }
 template <int POL, bool PUSH, bool CW>
-__global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, int32_t* W, int32_t* Wout) {
+__global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, WE* W, WE* Wout) {
   Work wk;
   wk.zero();
   Bins b;
