@@ -101,7 +101,10 @@ typedef struct gc_opts {
   float* kernel_ms;          /* optional host pointer: device time (CUDA events on the call's
                                 stream) from the first to the last colouring kernel, i.e.
                                 excluding argument checks, copies and validation */
-  uint64_t reserved[3];
+  uint64_t* phase_ns;        /* optional host pointer [2 * trace_capacity + 1] (diagnostics, with
+                                GC_FLAG_TRACE): device globaltimer (ns) after the ingest and
+                                after Phase A / Phase B of every round, persistent driver only */
+  uint64_t reserved[2];
 } gc_opts;
 
 /* Fill *o with the defaults above (policy HIGHER_ID, flags GC_FLAG_VALIDATE). */

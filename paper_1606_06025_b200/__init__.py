@@ -56,7 +56,7 @@ class Opts(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("trace_worklist", ctypes.c_void_p),
                 ("trace_capacity", ctypes.c_uint32), ("group_bin_max", ctypes.c_uint32),
                 ("work", ctypes.POINTER(Work)), ("kernel_ms", ctypes.POINTER(ctypes.c_float)),
-                ("reserved", ctypes.c_uint64 * 3)]
+                ("phase_ns", ctypes.c_void_p), ("reserved", ctypes.c_uint64 * 2)]
 
 
 _vp = ctypes.c_void_p
@@ -104,6 +104,7 @@ class ColorResult:
     trace: list | None = None
     work: dict | None = field(default=None)
     kernel_ms: float | None = None
+    phase_us: list | None = None     # per round (Phase A us, Phase B us) with phase_times=True
 
 
 def default_opts() -> Opts:
@@ -116,7 +117,8 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
           symmetry: bool = False, pull_firstfit: bool = False, host_rounds: bool = False,
           trace: bool = False, count_work: bool = False, max_rounds: int = 0,
           thread_bin_max: int = 0, group_bin_max: int = 0, warp_bin_max: int = 0, blocks_per_sm: int = 0,
-          stream=None, device: int | None = None, out=None, time_kernel: bool = False) -> ColorResult:
+          stream=None, device: int | None = None, out=None, time_kernel: bool = False,
+          phase_times: bool = False) -> ColorResult:
     """gc_color(n, row_ptr, col_idx, opts, colors_out, &num_colors, &rounds) (include/gc.h).
 
     row_ptr: int64[n+1], col_idx: int32[m] — torch tensors (CUDA or CPU) or numpy arrays.
@@ -125,6 +127,7 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
     """
     import numpy as np
     n = int(row_ptr.shape[0]) - 1
+    trace = trace or phase_times
     o = default_opts()
     o.policy = POLICIES[policy]
     o.flags = ((FLAG_VALIDATE if validate else 0) | (FLAG_VALIDATE_SYMMETRY if symmetry else 0)
@@ -150,6 +153,10 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
             out = np.zeros(max(n, 1), dtype=np.uint32)
     o.stream = stream
     tr = None
+    ph = None
+    if phase_times:
+        ph = np.zeros(2 * max(n + 2, 1) + 1, dtype=np.uint64)
+        o.phase_ns = ph.ctypes.data
     if trace:
         tr = np.zeros(max(n + 2, 1), dtype=np.uint32)
         o.trace_worklist = tr.ctypes.data
@@ -172,6 +179,10 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
         res.work = wk.as_dict()
     if time_kernel:
         res.kernel_ms = float(kms.value)
+    if phase_times:
+        t = ph[:2 * rd.value + 1].astype(np.int64)
+        res.phase_us = [((t[2 * r + 1] - t[2 * r]) / 1e3 if r > 0 else 0.0, (t[2 * r + 2] - t[2 * r + 1]) / 1e3)
+                        for r in range(rd.value)]
     return res
 
 

@@ -332,9 +332,12 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   // ---- workspace
   const bool push = !(o.flags & GC_FLAG_PULL_FIRSTFIT);
   const bool cw = (o.flags & GC_FLAG_COUNT_WORK) != 0;
-  void *st, *fm = nullptr, *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
+  void *st, *fm = nullptr, *fm2 = nullptr, *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
   CK(sc.alloc(&st, sizeof(uint32_t) * (size_t)n));
-  if (push) CK(sc.alloc(&fm, sizeof(uint32_t) * (size_t)n));
+  if (push) {
+    CK(sc.alloc(&fm, sizeof(uint32_t) * (size_t)n));
+    CK(sc.alloc(&fm2, sizeof(uint32_t) * (size_t)n));
+  }
   CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&w1, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&info, sizeof(DevInfo)));
@@ -370,11 +373,18 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.ci = d_ci;
   p.st = (uint32_t*)st;
   p.fm = (uint32_t*)fm;
+  p.fm2 = (uint32_t*)fm2;
   p.wl0 = (WE*)w0;
   p.wl1 = (WE*)w1;
   p.info = (DevInfo*)info;
   p.trace = (uint32_t*)dtrace;
   p.trace_cap = trace ? o.trace_capacity : 0;
+  void* dphase = nullptr;
+  if (trace && o.phase_ns) {
+    CK(sc.alloc(&dphase, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1)));
+    CK(cudaMemsetAsync(dphase, 0, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1), s));
+    p.phase_ns = (unsigned long long*)dphase;
+  }
   p.colors_out = (uint32_t*)dcol;
   p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
   p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
@@ -519,6 +529,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       CK(cudaMemcpyAsync(o.trace_worklist, dtrace, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
     }
+  }
+  if (dphase) {
+    CK(cudaMemcpyAsync(o.phase_ns, dphase, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   }
   if (cw) {
     memset(o.work, 0, sizeof(gc_work));

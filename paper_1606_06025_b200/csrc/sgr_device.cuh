@@ -21,10 +21,11 @@
 //     only sets the top bit of its own vertex — so no phase uses a bit written in the same
 //     phase (aligned words are single-copy atomic) and no locks are needed.  16-bit words
 //     halve the gather footprint so it stays resident in the 126 MB L2.
-//   * Incremental forbidden-colour mask fm[v] (colours 1..32): committed colours never
-//     change, so a committing vertex REDs its colour bit into fm of every neighbour (one RED
-//     per directed edge over the whole run) and Phase A is O(1): tent = ffs(~fm[v]); only a
-//     full mask falls back to the exact windowed scan from colour 33 (reading C7).
+//   * Incremental forbidden-colour masks fm[v] (colours 1..32, hot) and fm2[v] (33..64, cold):
+//     committed colours never change, so a committing vertex REDs its colour bit into the
+//     mask of every neighbour (one RED per directed edge over the whole run) and Phase A is
+//     O(1): tent = ffs(~fm[v]) (or 32 + ffs(~fm2[v])); only colours beyond 64 fall back to
+//     the exact windowed scan from colour 65 (reading C7).
 //     GC_FLAG_PULL_FIRSTFIT selects the paper's full rescan instead (same result).
 //   * L1 policy: the read-only CSR goes through the non-coherent path without allocating
 //     in L1; everything written during the run is read L2-coherently (.cg).
@@ -93,11 +94,13 @@ struct Params {
   const int32_t* __restrict__ ci;
   void* st;                     // state word per vertex (uint16_t or uint32_t)
   uint32_t* fm;                 // forbidden colours 1..32 per vertex (incremental mode)
+  uint32_t* fm2;                // forbidden colours 33..64 (cold: only touched by colours > 32)
   WE* wl0;                      // worklist buffers, n entries each, bin segments
   WE* wl1;
   DevInfo* info;
   uint32_t* trace;
   uint32_t trace_cap;
+  unsigned long long* phase_ns;  // diagnostics: [0] = after ingest, [2r-1] after A(r), [2r] after B(r)
   uint32_t* colors_out;
   uint32_t max_rounds;
   uint32_t t1;                  // degree <= t1: one thread per vertex
@@ -558,20 +561,22 @@ __device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_
 }
 
 // ---------------------------------------------------------------- commit scatter
-// A winner ORs its colour bit into the forbidden mask of every neighbour: entries
+// A winner ORs its colour bit (colours 1..64) into the forbidden mask of every neighbour: entries
 // e = start, start+STEP, ... < end; four col_idx loads are issued before the four
 // fire-and-forget REDs so that each lane keeps several misses in flight.
 template <int STEP>
-__device__ __forceinline__ void scatter(const Params& p, uint32_t bit, int64_t start, int64_t end) {
+__device__ __forceinline__ void scatter(const Params& p, uint32_t color, int64_t start, int64_t end) {
+  uint32_t* const mask = color <= 32 ? p.fm : p.fm2;   // colour 1..64
+  const uint32_t bit = 1u << ((color - 1) & 31);
   int64_t e = start;
   for (; e + 3 * STEP < end; e += 4 * STEP) {
     const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + STEP), w2 = ldc(p.ci, e + 2 * STEP), w3 = ldc(p.ci, e + 3 * STEP);
-    red_or(p.fm + w0, bit);
-    red_or(p.fm + w1, bit);
-    red_or(p.fm + w2, bit);
-    red_or(p.fm + w3, bit);
+    red_or(mask + w0, bit);
+    red_or(mask + w1, bit);
+    red_or(mask + w2, bit);
+    red_or(mask + w3, bit);
   }
-  for (; e < end; e += STEP) red_or(p.fm + ldc(p.ci, e), bit);
+  for (; e < end; e += STEP) red_or(mask + ldc(p.ci, e), bit);
 }
 
 }  // namespace gcdev

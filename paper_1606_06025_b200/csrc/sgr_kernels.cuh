@@ -30,7 +30,10 @@ __device__ __forceinline__ void prologue_count(const Params& p) {
       if (sizeof(S) == 2 && deg > NARROW_MAX_DEG) wide = true;
       b = bin_of(p, deg);
       sts(st + v, 1u);
-      if (PUSH) sts(p.fm + v, 0u);
+      if (PUSH) {
+        sts(p.fm + v, 0u);
+        sts(p.fm2 + v, 0u);
+      }
     }
 #pragma unroll
     for (int k = 0; k < NBIN; ++k) {
@@ -100,14 +103,22 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, 
         v = ldw_v(Wb + i);
         f = ldf(p.fm + v);
       }
-      const bool fb = act && f == FULL;
-      if (act && !fb) sts(st + v, (uint32_t)__ffs(~f));
+      bool fb = false;
+      if (act) {
+        if (f != FULL) {
+          sts(st + v, (uint32_t)__ffs(~f));
+        } else {
+          const uint32_t f2 = ldf(p.fm2 + v);
+          if (f2 != FULL) sts(st + v, 32u + (uint32_t)__ffs(~f2));
+          else fb = true;
+        }
+      }
       unsigned m = __ballot_sync(FULL, fb);
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const int32_t u = __shfl_sync(FULL, v, src);
-        const uint32_t t = firstfit_warp<S, CW>(p, u, 33u, wk, lane);
+        const uint32_t t = firstfit_warp<S, CW>(p, u, 65u, wk, lane);
         if (lane == 0) sts(st + u, t);
       }
     }
@@ -203,9 +214,9 @@ __device__ __forceinline__ void phase_b_thread(const Params& p, const WE* Wb, ui
         lose = conflict_thread<S, POL, CW>(p, v, tent, sr.lo, sr.hi, sr.down, POL == DEGREE ? end - e.beg : 0, wk);
         if (!lose) {
           sts(st + v, tent | SW<S>::COMMIT);
-          if (PUSH && tent <= 32) {
+          if (PUSH && tent <= 64) {
             if (end < 0) end = ldr(p.rp, v + 1);
-            scatter<1>(p, 1u << (tent - 1), e.beg, end);
+            scatter<1>(p, tent, e.beg, end);
             if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
           }
         }
@@ -248,8 +259,8 @@ __device__ __forceinline__ void phase_b_group(const Params& p, const WE* Wb, uin
       const bool lose = conflict_group<S, G, POL, CW>(p, act, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, lane, wk);
       if (act && !lose) {
         if (gl == 0) sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 32) {
-          scatter<G>(p, 1u << (tent - 1), e.beg + gl, end);
+        if (PUSH && tent <= 64) {
+          scatter<G>(p, tent, e.beg + gl, end);
           if (CW && gl == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
         }
       }
@@ -306,8 +317,8 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
         }
       } else {
         if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 32) {
-          scatter<BLOCK>(p, 1u << (tent - 1), e.beg + threadIdx.x, end);
+        if (PUSH && tent <= 64) {
+          scatter<BLOCK>(p, tent, e.beg + threadIdx.x, end);
           if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
         }
       }
@@ -353,8 +364,11 @@ __device__ __forceinline__ void flush_work(const Params& p, Work& wk) {
 // ---------------------------------------------------------------- a4: persistent driver
 // One cooperative launch runs ingest, every round and finalize.  Per round: Phase A,
 // barrier, Phase B (+push), barrier; every CTA reads |W_{r+1}| and leaves together.
+#ifndef GC_MINB
+#define GC_MINB 4
+#endif
 template <class S, int POL, bool PUSH, bool CW>
-__global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
+__global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
   Work wk;
   wk.zero();
   prologue_count<S, PUSH>(p);
@@ -363,6 +377,8 @@ __global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
   bins.load(p);
   prologue_scatter(p, bins);
   if (!grid_sync(p)) return;
+  const bool stamp = p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0;
+  if (stamp) p.phase_ns[0] = globaltimer();
 
   // The worklist pointers are re-read from DevInfo every round instead of being swapped in
   // registers: with loop-carried pointer swaps, ptxas (12.9) was observed to reuse the
@@ -375,8 +391,10 @@ __global__ void __launch_bounds__(BLOCK) sgr_persistent(Params p) {
       phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
       if (!grid_sync(p)) return;
     }
+    if (stamp && r <= p.trace_cap) p.phase_ns[2 * r - 1] = globaltimer();
     phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
     if (!grid_sync(p)) return;
+    if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
     const uint32_t left = next_total(p, r);
     if (left == 0) break;
     if (r >= p.max_rounds) {

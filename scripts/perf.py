@@ -43,6 +43,15 @@ def main():
     variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
                          dict(host_rounds=True, pull_firstfit=True)]
     variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
+    if args.sweep == "phases":
+        res = gc.color(rp, ci, validate=False, phase_times=True)
+        tot_a = sum(a for a, b in res.phase_us)
+        tot_b = sum(b for a, b in res.phase_us)
+        print(json.dumps({"config": args.config, "rounds": res.rounds, "phaseA_us": round(tot_a, 1),
+                          "phaseB_us": round(tot_b, 1)}))
+        for r, ((a, b), w) in enumerate(zip(res.phase_us, res.trace), 1):
+            print(f"  r={r:3d} |W|={w:10d} A={a:9.1f}us B={b:9.1f}us")
+        return
     for kw in variants[args.sweep]:
         ts = []
         res = None
