@@ -88,15 +88,16 @@ typedef struct gc_opts {
   uint32_t flags;            /* GC_FLAG_*; default GC_FLAG_VALIDATE */
   uint32_t max_rounds;       /* 0 -> n + 1 (reading C13) */
   int32_t device;            /* CUDA ordinal; -1 = the calling thread's current device */
-  uint32_t thread_bin_max;   /* degree <= this -> one thread per vertex (0 -> default 16) */
-  uint32_t warp_bin_max;     /* degree <= this (and > group_bin_max) -> one warp per vertex
-                                (0 -> default 4096);
-                                larger degrees -> one CTA per vertex */
+  uint32_t thread_bin_max;   /* a winner of degree <= this scatters its colour bit by itself,
+                                larger ones with the whole warp (0 -> default 32) */
+  uint32_t warp_bin_max;     /* degree <= this -> thread probe + warp continuation per vertex
+                                (0 -> default 4096); larger degrees -> one CTA per vertex
+                                (load balancing) */
   uint32_t blocks_per_sm;    /* persistent grid = SMs x this (0 -> max co-resident) */
   void* stream;              /* cudaStream_t to run on; NULL = library-internal stream */
   uint32_t* trace_worklist;  /* host or device, [trace_capacity]; used with GC_FLAG_TRACE */
   uint32_t trace_capacity;
-  uint32_t group_bin_max;    /* degree <= this -> one 8-lane group per vertex (0 -> default 128) */
+  uint32_t group_bin_max;    /* reserved (ignored) */
   gc_work* work;             /* host pointer; used with GC_FLAG_COUNT_WORK */
   float* kernel_ms;          /* optional host pointer: device time (CUDA events on the call's
                                 stream) from the first to the last colouring kernel, i.e.

@@ -8,8 +8,9 @@
 //              atomics (§3.1 "Atomic Operation Reduction");
 //   rounds   = Data-GC (Alg. 7), double-buffered worklists, ONE
 //              persistent kernel with a device-wide barrier (§3.3 "Kernel Fusion");
-//   binning  = thread / 8-lane group / warp / CTA per vertex by degree (§3.3 "Load
-//              Balancing");
+//   load balancing (§3.3 "Load Balancing"): every vertex is first probed by its own
+//              thread; the few that need a long scan or a large scatter are continued by the
+//              whole warp; degrees above a threshold get a CTA;
 //   CSR read through the non-coherent read-only path (§3.3 "Read-only Data Caching").
 //
 // B200-first differences from the paper's K40c design:
@@ -37,7 +38,8 @@
 
 namespace gcdev {
 
-constexpr int NBIN = 4;            // 0 = thread, 1 = 8-lane group, 2 = warp, 3 = CTA per vertex
+constexpr int NBIN = 2;            // 0 = thread probe + warp continuation, 1 = CTA per vertex
+constexpr int PROBE = 4;           // Phase-B positions a vertex's own thread examines first
 constexpr int PBUF = 64;           // per-warp push staging entries per bin
 constexpr int BLOCK = 256;
 constexpr int WARPS = BLOCK / 32;
@@ -103,9 +105,8 @@ struct Params {
   unsigned long long* phase_ns;  // diagnostics: [0] = after ingest, [2r-1] after A(r), [2r] after B(r)
   uint32_t* colors_out;
   uint32_t max_rounds;
-  uint32_t t1;                  // degree <= t1: one thread per vertex
-  uint32_t t2;                  // degree <= t2: one 8-lane group per vertex
-  uint32_t t3;                  // degree <= t3: one warp per vertex; above: one CTA
+  uint32_t t1;                  // winners of degree <= t1 scatter by themselves, larger: warp-wide
+  uint32_t t3;                  // degree <= t3: bin 0 (thread + warp); above: bin 1 (one CTA)
   unsigned long long timeout_ns;
 };
 
@@ -246,9 +247,7 @@ __device__ __noinline__ bool grid_sync(const Params& p) {
 
 // ---------------------------------------------------------------- bins
 
-__device__ __forceinline__ int bin_of(const Params& p, int64_t deg) {
-  return deg <= (int64_t)p.t1 ? 0 : deg <= (int64_t)p.t2 ? 1 : deg <= (int64_t)p.t3 ? 2 : 3;
-}
+__device__ __forceinline__ int bin_of(const Params& p, int64_t deg) { return deg <= (int64_t)p.t3 ? 0 : 1; }
 
 // Offsets of the bin segments inside each worklist buffer (fixed for the whole run).
 struct Bins {
@@ -318,8 +317,6 @@ struct Pusher {
   template <bool CW>
   __device__ __forceinline__ void flush(int lane, unsigned long long& pushed) {
     flush_bin<0, CW>(lane, pushed);
-    flush_bin<1, CW>(lane, pushed);
-    flush_bin<2, CW>(lane, pushed);
   }
 };
 
@@ -453,84 +450,6 @@ __device__ __forceinline__ int32_t row_split(const Params& p, int32_t v, int64_t
     else hi = mid;
   }
   return (int32_t)(lo - beg);
-}
-
-template <class S, int POL, bool CW>
-__device__ __forceinline__ bool conflict_thread(const Params& p, int32_t v, uint32_t tent, int64_t lo, int64_t hi,
-                                                bool down, int64_t dv, Work& wk) {
-  const S* st = (const S*)p.st;
-  constexpr uint32_t CM = SW<S>::CMASK;
-  const int64_t len = hi - lo;
-  int64_t j = 0;
-  for (; j + 4 <= len; j += 4) {
-    const int64_t e = down ? hi - 1 - j : lo + j;
-    const int64_t d = down ? -1 : 1;
-    const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + d), w2 = ldc(p.ci, e + 2 * d), w3 = ldc(p.ci, e + 3 * d);
-    const uint32_t c0 = lds(st + w0) & CM, c1 = lds(st + w1) & CM, c2 = lds(st + w2) & CM, c3 = lds(st + w3) & CM;
-    const bool h0 = c0 == tent && recolors<POL>(p, v, w0, dv);
-    const bool h1 = c1 == tent && recolors<POL>(p, v, w1, dv);
-    const bool h2 = c2 == tent && recolors<POL>(p, v, w2, dv);
-    const bool h3 = c3 == tent && recolors<POL>(p, v, w3, dv);
-    if (h0 | h1 | h2 | h3) {
-      if (CW) {
-        const int f = h0 ? 1 : h1 ? 2 : h2 ? 3 : 4;
-        wk.v[W_B_EDGE] += j + f;
-        wk.v[W_B_GATHER] += j + f;
-      }
-      return true;
-    }
-  }
-  for (; j < len; ++j) {
-    const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
-    if ((lds(st + w) & CM) == tent && recolors<POL>(p, v, w, dv)) {
-      if (CW) { wk.v[W_B_EDGE] += j + 1; wk.v[W_B_GATHER] += j + 1; }
-      return true;
-    }
-  }
-  if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
-  return false;
-}
-
-// Group scan: a group of G lanes (G = 8 or 32, aligned in the warp) examines G positions of
-// its range per step.  Called by the whole warp in lockstep (warp-uniform loop); inactive
-// groups pass act = false.  Returns the group's verdict in every lane of the group.
-template <class S, int G, int POL, bool CW>
-__device__ __forceinline__ bool conflict_group(const Params& p, bool act, int32_t v, uint32_t tent, int64_t lo,
-                                               int64_t hi, bool down, int64_t dv, int lane, Work& wk) {
-  const S* st = (const S*)p.st;
-  const int gl = lane % G;
-  const int shift = (lane / G) * G;
-  const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << shift);
-  const int64_t len = act ? hi - lo : 0;
-  bool done = len <= 0;
-  bool lose = false;
-  for (int64_t k = 0;; k += G) {
-    if (__all_sync(FULL, done)) break;
-    bool hit = false, valid = false;
-    if (!done) {
-      const int64_t j = k + gl;
-      valid = j < len;
-      if (valid) {
-        const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
-        hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
-      }
-    }
-    const unsigned hb = __ballot_sync(FULL, hit) & gmask;
-    if (CW) {
-      const unsigned vb = __ballot_sync(FULL, valid) & gmask;
-      if (!done && gl == 0) {
-        const int f = hb ? __ffs(hb >> shift) - 1 : G - 1;  // the sequential scan stops here
-        const unsigned upto = (f >= 31 ? FULL : ((2u << f) - 1u)) << shift;
-        wk.v[W_B_EDGE] += __popc(vb & upto);
-        wk.v[W_B_GATHER] += __popc(vb & upto);
-      }
-    }
-    if (!done) {
-      if (hb) { lose = true; done = true; }
-      else if (k + G >= len) done = true;
-    }
-  }
-  return lose;
 }
 
 template <class S, int POL, bool CW>

@@ -125,7 +125,8 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, 
   }
 }
 
-// Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round.
+// Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round;
+// bin 0: degree <= 32 by the vertex's own thread, larger by the whole warp; bin 1: one CTA.
 template <class S, bool CW>
 __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, const WE* W, const uint32_t* nb,
                                              Work& wk, uint32_t* s_win) {
@@ -134,23 +135,29 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
   const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
   {
     const WE* Wb = W + bins.off[0];
-    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nb[0]; i += gridDim.x * BLOCK) {
-      const int32_t v = ldw_v(Wb + i);
-      sts(st + v, firstfit_thread<S, CW>(p, v, 1u, wk));
-    }
-  }
-#pragma unroll
-  for (int b = 1; b <= 2; ++b) {
-    const WE* Wb = W + bins.off[b];
-    for (uint32_t i = gw; i < nb[b]; i += nw) {
-      const int32_t v = ldw_v(Wb + i);
-      const uint32_t t = firstfit_warp<S, CW>(p, v, 1u, wk, lane);
-      if (lane == 0) sts(st + v, t);
+    for (uint32_t base = gw * 32; base < nb[0]; base += nw * 32) {
+      const uint32_t i = base + lane;
+      bool big = false;
+      WE e;
+      if (i < nb[0]) {
+        e = ldw(Wb + i);
+        const int64_t deg = ldr(p.rp, e.v + 1) - e.beg;
+        if (deg <= 32) sts(st + e.v, firstfit_thread<S, CW>(p, e.v, 1u, wk));
+        else big = true;
+      }
+      unsigned m = __ballot_sync(FULL, big);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t u = __shfl_sync(FULL, e.v, src);
+        const uint32_t t = firstfit_warp<S, CW>(p, u, 1u, wk, lane);
+        if (lane == 0) sts(st + u, t);
+      }
     }
   }
   {
-    const WE* Wb = W + bins.off[3];
-    for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
+    const WE* Wb = W + bins.off[1];
+    for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       const int32_t v = ldw_v(Wb + i);
       const uint32_t t = firstfit_cta<S, CW>(p, v, 1u, wk, s_win);
       if (threadIdx.x == 0) sts(st + v, t);
@@ -171,7 +178,7 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
     p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
   }
-  if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1] + nb[2] + nb[3];
+  if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
   if (PUSH) phase_a_mask<S, CW>(p, bins, W, nb, wk);
   else phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
 }
@@ -180,7 +187,6 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
 // Winners commit (set the top bit of their own word) and, in mask mode, OR their colour bit
 // into the forbidden mask of every neighbour; losers go to W_out through the Pusher.
 
-// bin 0: one vertex per lane
 // Warps pop chunks of CH items from a per-bin queue head (one atomic per chunk) so that
 // costly items (long scans) do not leave the rest of the grid idle at the phase barrier.
 template <uint32_t CH>
@@ -190,81 +196,120 @@ __device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, int lane) {
   return __shfl_sync(FULL, b, 0);
 }
 
+// Position of the j-th entry of a scan range in scan order.
+__device__ __forceinline__ int64_t scan_pos(int64_t lo, int64_t hi, bool down, int64_t j) {
+  return down ? hi - 1 - j : lo + j;
+}
+
+// bin 0.  Stage 1: each lane takes one vertex and examines the first PROBE positions of its
+// scan range (independent loads: ILP).  Most losers are decided here (the nearest lower ids
+// are the likeliest conflicts).  Stage 2: the vertices whose range is longer and still
+// undecided are continued one after the other by the whole warp, 32 positions per step
+// (coalesced col_idx, 32 gathers in flight).  Winners commit; a winner of degree > t1 has its
+// forbidden-mask scatter done by the whole warp as well.
 template <class S, int POL, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_b_thread(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
-                                               Work& wk) {
+__device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
+                                             Work& wk) {
   S* st = (S*)p.st;
+  constexpr uint32_t CM = SW<S>::CMASK;
   const int lane = threadIdx.x & 31;
   constexpr uint32_t CH = 64;
   for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
     const uint32_t cend = min(c0 + CH, cnt);
     for (uint32_t base = c0; base < cend; base += 32) {
       const uint32_t i = base + lane;
-      bool lose = false;
-      WE e;
-      if (i < cnt) {
-        e = ldw(Wb + i);
-        const int32_t v = e.v;
-        const uint32_t tent = lds(st + v) & SW<S>::CMASK;
-        // the row end is needed for the split (first visit), the upper range and the scatter
-        int64_t end = -1;
-        if (e.k < 0 || POL != HIGHER_ID) end = ldr(p.rp, v + 1);
-        if (e.k < 0 && POL != DEGREE) e.k = row_split(p, v, e.beg, end);
-        const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-        lose = conflict_thread<S, POL, CW>(p, v, tent, sr.lo, sr.hi, sr.down, POL == DEGREE ? end - e.beg : 0, wk);
-        if (!lose) {
-          sts(st + v, tent | SW<S>::COMMIT);
-          if (PUSH && tent <= 64) {
-            if (end < 0) end = ldr(p.rp, v + 1);
-            scatter<1>(p, tent, e.beg, end);
-            if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
-          }
-        }
-      }
-      pu.template push<0, CW>(lose, e, lane, wk.v[W_PUSH]);
-    }
-  }
-}
-
-// bins 1 and 2: one G-lane group per vertex (G = 8 or 32)
-template <class S, int G, int B, int POL, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_b_group(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
-                                              Work& wk) {
-  S* st = (S*)p.st;
-  constexpr int PER = 32 / G;
-  constexpr uint32_t CH = 8 * PER;
-  const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
-  const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << (grp * G));
-  for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
-    const uint32_t cend = min(c0 + CH, cnt);
-    for (uint32_t base = c0; base < cend; base += PER) {
-      const uint32_t i = base + grp;
-      const bool act = i < cnt;
       WE e;
       e.v = 0;
       e.k = 0;
       e.beg = 0;
       uint32_t tent = 0;
-      int64_t end = 0;
-      if (act) {
+      int64_t end = -1, lo = 0, hi = 0, dv = 0;
+      bool down = true;
+      int state = 0;  // 0 inactive, 1 lose, 2 win, 3 undecided
+      if (i < cend) {
         e = ldw(Wb + i);
-        tent = lds(st + e.v) & SW<S>::CMASK;
-        end = ldr(p.rp, e.v + 1);
-        // first visit: the group leader finds the split, then shares it
-        if (e.k < 0 && POL != DEGREE && gl == 0) e.k = row_split(p, e.v, e.beg, end);
-      }
-      e.k = __shfl_sync(FULL, e.k, lane & ~(G - 1));
-      (void)gmask;
-      const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-      const bool lose = conflict_group<S, G, POL, CW>(p, act, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, lane, wk);
-      if (act && !lose) {
-        if (gl == 0) sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 64) {
-          scatter<G>(p, tent, e.beg + gl, end);
-          if (CW && gl == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+        tent = lds(st + e.v) & CM;
+        if (e.k < 0 || POL != HIGHER_ID) end = ldr(p.rp, e.v + 1);
+        if (e.k < 0 && POL != DEGREE) e.k = row_split(p, e.v, e.beg, end);
+        const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+        lo = sr.lo;
+        hi = sr.hi;
+        down = sr.down;
+        if (POL == DEGREE) dv = end - e.beg;
+        const int64_t len = hi - lo;
+        int32_t w[PROBE];
+        uint32_t c[PROBE];
+#pragma unroll
+        for (int u = 0; u < PROBE; ++u) w[u] = u < len ? ldc(p.ci, scan_pos(lo, hi, down, u)) : 0;
+#pragma unroll
+        for (int u = 0; u < PROBE; ++u) c[u] = u < len ? (lds(st + w[u]) & CM) : 0u;
+        int f = -1;
+#pragma unroll
+        for (int u = PROBE - 1; u >= 0; --u)
+          if (u < len && c[u] == tent && recolors<POL>(p, e.v, w[u], dv)) f = u;
+        if (f >= 0) state = 1;
+        else state = len <= PROBE ? 2 : 3;
+        if (CW && state != 3) {
+          const int64_t ex = f >= 0 ? f + 1 : (len < PROBE ? len : PROBE);
+          wk.v[W_B_EDGE] += ex;
+          wk.v[W_B_GATHER] += ex;
         }
       }
-      pu.template push<B, CW>(act && lose && gl == 0, e, lane, wk.v[W_PUSH]);
+      // stage 2: warp-wide continuation
+      unsigned und = __ballot_sync(FULL, state == 3);
+      while (und) {
+        const int src = __ffs(und) - 1;
+        und &= und - 1;
+        const int32_t v = __shfl_sync(FULL, e.v, src);
+        const uint32_t t = __shfl_sync(FULL, tent, src);
+        const int64_t slo = __shfl_sync(FULL, lo, src), shi = __shfl_sync(FULL, hi, src);
+        const int64_t sdv = __shfl_sync(FULL, dv, src);
+        const bool sdown = __shfl_sync(FULL, (int)down, src) != 0;
+        const int64_t len = shi - slo;
+        bool found = false;
+        int64_t examined = PROBE;
+        for (int64_t kk = PROBE; kk < len; kk += 32) {
+          const int64_t j = kk + lane;
+          bool hit = false;
+          if (j < len) {
+            const int32_t wv = ldc(p.ci, scan_pos(slo, shi, sdown, j));
+            hit = (lds(st + wv) & CM) == t && recolors<POL>(p, v, wv, sdv);
+          }
+          const unsigned hb = __ballot_sync(FULL, hit);
+          if (hb) {
+            found = true;
+            examined = kk + __ffs(hb);
+            break;
+          }
+          examined = kk + 32 < len ? kk + 32 : len;
+        }
+        if (lane == src) {
+          state = found ? 1 : 2;
+          if (CW) { wk.v[W_B_EDGE] += examined; wk.v[W_B_GATHER] += examined; }
+        }
+      }
+      // winners commit; masks of their neighbours get their colour bit
+      bool big = false;
+      if (state == 2) {
+        sts(st + e.v, tent | SW<S>::COMMIT);
+        if (PUSH && tent <= 64) {
+          if (end < 0) end = ldr(p.rp, e.v + 1);
+          if (end - e.beg <= (int64_t)p.t1) scatter<1>(p, tent, e.beg, end);
+          else big = true;
+          if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+        }
+      }
+      if (PUSH) {
+        unsigned bm = __ballot_sync(FULL, big);
+        while (bm) {
+          const int src = __ffs(bm) - 1;
+          bm &= bm - 1;
+          const uint32_t t = __shfl_sync(FULL, tent, src);
+          const int64_t sb = __shfl_sync(FULL, e.beg, src), se = __shfl_sync(FULL, end, src);
+          scatter<32>(p, t, sb + lane, se);
+        }
+      }
+      pu.template push<0, CW>(state == 1, e, lane, wk.v[W_PUSH]);
     }
   }
 }
@@ -282,23 +327,21 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1] + nb[2] + nb[3];
-    if (CW) wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1] + nb[2] + nb[3];
+    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1];
+    if (CW) wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1];
   }
   uint32_t* cnt_next = &p.info->cnt[nxt][0];
   Pusher pu;
   pu.init(s_pbuf[warp], Wout, cnt_next, bins);
 
-  phase_b_thread<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
-  phase_b_group<S, 8, 1, POL, PUSH, CW>(p, W + bins.off[1], nb[1], &p.info->qctr[cur][1][0], pu, wk);
-  phase_b_group<S, 32, 2, POL, PUSH, CW>(p, W + bins.off[2], nb[2], &p.info->qctr[cur][2][0], pu, wk);
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
   pu.template flush<CW>(lane, wk.v[W_PUSH]);
 
-  // bin 3: one CTA per vertex (rare, huge degrees): direct push
+  // bin 1: one CTA per vertex (huge degrees): direct push
   {
-    const WE* Wb = W + bins.off[3];
-    WE* Ob = Wout + bins.off[3];
-    for (uint32_t i = blockIdx.x; i < nb[3]; i += gridDim.x) {
+    const WE* Wb = W + bins.off[1];
+    WE* Ob = Wout + bins.off[1];
+    for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       WE e = ldw(Wb + i);
       const uint32_t tent = lds(st + e.v) & SW<S>::CMASK;
       const int64_t end = ldr(p.rp, e.v + 1);
@@ -312,7 +355,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
       const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, &s_first);
       if (lose) {
         if (threadIdx.x == 0) {
-          stw(Ob + atomicAdd(&cnt_next[3], 1u), e);
+          stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
           if (CW) wk.v[W_PUSH] += 1;
         }
       } else {
@@ -330,8 +373,10 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
 // |W_{r+1}| summed over bins (read after the barrier that ends Phase B of round r).
 __device__ __forceinline__ uint32_t next_total(const Params& p, uint32_t r) {
   const uint32_t nxt = (r + 1) % 3;
-  return ld_relaxed(&p.info->cnt[nxt][0]) + ld_relaxed(&p.info->cnt[nxt][1]) + ld_relaxed(&p.info->cnt[nxt][2]) +
-         ld_relaxed(&p.info->cnt[nxt][3]);
+  uint32_t t = 0;
+#pragma unroll
+  for (int b = 0; b < NBIN; ++b) t += ld_relaxed(&p.info->cnt[nxt][b]);
+  return t;
 }
 
 // ---------------------------------------------------------------- a5: finalize
