@@ -24,7 +24,7 @@ UNIT = "GTEPS"
 
 # bounded CPU-oracle samples of each workload family (~10-30 s of single-core CPU work)
 CPU_SAMPLES = {
-    "rmat24": ("rmat", dict(scale=21, edge_factor=16)),
+    "rmat24": ("rmat", dict(scale=22, edge_factor=16)),
     "rmat16": ("rmat", dict(scale=16, edge_factor=8)),
     "stencil128": ("stencil", dict(nx=96)),
     "mesh8192": ("mesh", dict(rows=4096, cols=4096, p_delete=0.3)),
@@ -110,16 +110,29 @@ class ClockSampler:
                 "samples": len(s)}
 
 
-def algorithmic_bytes(work, n):
-    """Bytes the implemented algorithm must move per launch (DESIGN.md §7 per-unit table)."""
-    return (44 * n                                   # ingest: row_ptr x2, st, fm, W_1
-            + 12 * work["phase_a_vertices"]          # W id, fm read, st write
-            + 8 * work["phase_a_edges"]              # fallback First-Fit: col + st gather
-            + 28 * work["phase_b_vertices"]          # W id, row_ptr pair, own st, commit/push
-            + 4 * work["phase_b_edges"]              # col_idx entries scanned
-            + 4 * work["phase_b_gathers"]            # neighbour colour gathers
-            + 8 * work["commit_scatter"]             # col + forbidden-mask RED
-            + 8 * n)                                 # finalize: st read, colours write
+def algorithmic_bytes(work, n, narrow=True):
+    """Bytes the implemented algorithm must move per launch (DESIGN.md §7 per-unit table).
+
+    Per-unit figures (sw = state word, 2 B for Delta < 32767 else 4 B; WE = 16-B worklist
+    entry {v, split, row start}):
+      ingest      per vertex   : 2x row_ptr pair (32) + sw + fm + fm2 (8) + WE write (16)
+      Phase A     per vertex   : v (4) + fm (4) + sw write
+                  per fallback neighbour : col (4) + sw
+      Phase B     per vertex   : WE (16) + own sw + row_ptr end (8)
+                  per examined position  : col (4) + sw gather
+                  per loser    : WE push (16);  per winner : sw commit
+      scatter     per edge     : col (4) + forbidden-mask RED (4)
+      finalize    per vertex   : sw read + colour write (4)
+    """
+    sw = 2 if narrow else 4
+    losers = work["pushes"]
+    winners = work["phase_b_vertices"] - losers
+    return ((32 + sw + 8 + 16) * n
+            + (8 + sw) * work["phase_a_vertices"] + (4 + sw) * work["phase_a_edges"]
+            + (16 + sw + 8) * work["phase_b_vertices"] + (4 + sw) * work["phase_b_edges"]
+            + 16 * losers + sw * winners
+            + 8 * work["commit_scatter"]
+            + (sw + 4) * n)
 
 
 def measured_peaks():
@@ -190,7 +203,7 @@ def run_ours(args):
     # untimed instrumented run: exact work counters -> algorithmic bytes per launch
     wres = gc.color(rp, ci, count_work=True, trace=True, **kw)
     work = wres.work
-    alg_bytes = algorithmic_bytes(work, n)
+    alg_bytes = algorithmic_bytes(work, n, narrow=g.max_degree() < 32767)
     verified = gc.verify(rp, ci, out) == -1
 
     for _ in range(args.warmup):

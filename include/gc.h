@@ -89,9 +89,9 @@ typedef struct gc_opts {
   uint32_t max_rounds;       /* 0 -> n + 1 (reading C13) */
   int32_t device;            /* CUDA ordinal; -1 = the calling thread's current device */
   uint32_t thread_bin_max;   /* a winner of degree <= this scatters its colour bit by itself,
-                                larger ones with the whole warp (0 -> default 32) */
+                                larger ones with the whole warp (0 -> default 16) */
   uint32_t warp_bin_max;     /* degree <= this -> thread probe + warp continuation per vertex
-                                (0 -> default 4096); larger degrees -> one CTA per vertex
+                                (0 -> default 512); larger degrees -> one CTA per vertex
                                 (load balancing) */
   uint32_t blocks_per_sm;    /* persistent grid = SMs x this (0 -> max co-resident) */
   void* stream;              /* cudaStream_t to run on; NULL = library-internal stream */

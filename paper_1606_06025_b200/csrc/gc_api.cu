@@ -393,8 +393,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   }
   p.colors_out = (uint32_t*)dcol;
   p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
-  p.t1 = o.thread_bin_max ? o.thread_bin_max : 32;
-  p.t3 = o.warp_bin_max ? o.warp_bin_max : 4096;
+  p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
+  p.t3 = o.warp_bin_max ? o.warp_bin_max : 512;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
   p.timeout_ns = 60ull * 1000000000ull;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -334,10 +334,8 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   Pusher pu;
   pu.init(s_pbuf[warp], Wout, cnt_next, bins);
 
-  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
-  pu.template flush<CW>(lane, wk.v[W_PUSH]);
-
-  // bin 1: one CTA per vertex (huge degrees): direct push
+  // bin 1 first (one CTA per vertex, high degrees: the longest items start early), then the
+  // dynamic bin-0 queue fills the gaps
   {
     const WE* Wb = W + bins.off[1];
     WE* Ob = Wout + bins.off[1];
@@ -368,6 +366,8 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
       __syncthreads();
     }
   }
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
+  pu.template flush<CW>(lane, wk.v[W_PUSH]);
 }
 
 // |W_{r+1}| summed over bins (read after the barrier that ends Phase B of round r).

@@ -37,8 +37,8 @@ def main():
     ref_c = ref.colors.clone()
 
     variants = {"default": [dict()]}
-    variants["bins"] = [dict(thread_bin_max=t1, group_bin_max=t2, warp_bin_max=t3)
-                        for t1 in (8, 16, 24, 32) for t2 in (64, 128, 256) for t3 in (4096,)]
+    variants["bins"] = [dict(thread_bin_max=t1, warp_bin_max=t3)
+                        for t1 in (16, 32, 64) for t3 in (128, 256, 512, 1024, 4096)]
     variants["grid"] = [dict(blocks_per_sm=b) for b in (1, 2, 3, 4, 5, 6, 8)]
     variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
                          dict(host_rounds=True, pull_firstfit=True)]
