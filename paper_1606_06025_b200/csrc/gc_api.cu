@@ -699,3 +699,7 @@ gc_status gc__bench_grid_sync(int32_t device, int32_t blocks_per_sm, int32_t ite
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- multi-GPU partitions
+#include "../../include/gc_dist.h"
+#include "dist_api.cuh"

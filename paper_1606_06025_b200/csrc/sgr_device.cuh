@@ -91,7 +91,8 @@ struct __align__(16) WE {
 };
 
 struct Params {
-  int32_t n;
+  int32_t n;                    // rows held here (all vertices, or one partition's range)
+  int32_t v_base;               // global id of local row 0 (0 on one GPU); st is global-indexed
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;
   void* st;                     // state word per vertex (uint16_t or uint32_t)
@@ -138,6 +139,9 @@ __device__ __forceinline__ int64_t ldr(const int64_t* __restrict__ p, int64_t i)
 // ld.global.cg (L2 only, never L1): with L1-cacheable weak loads of the state words the
 // host-driven ablation (one launch per phase) was observed to read stale lines across
 // kernel boundaries on this B200/driver; .cg costs nothing measurable.
+// Row offsets of (global) vertex v held in this partition.
+#define RP(p, v) ldr((p).rp, (int64_t)(v) - (p).v_base)
+
 // Worklists: written in one phase, read after a barrier, streamed.
 __device__ __forceinline__ WE ldw(const WE* p) {
   WE e;
@@ -327,7 +331,7 @@ struct Pusher {
 template <class S, bool CW>
 __device__ __forceinline__ uint32_t firstfit_thread(const Params& p, int32_t v, uint32_t base, Work& wk) {
   const S* st = (const S*)p.st;
-  const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+  const int64_t beg = RP(p, v), end = RP(p, v + 1);
   for (;;) {
     unsigned long long mask = 0;
     int64_t e = beg;
@@ -355,7 +359,7 @@ __device__ __forceinline__ uint32_t firstfit_thread(const Params& p, int32_t v, 
 template <class S, bool CW>
 __device__ __forceinline__ uint32_t firstfit_warp(const Params& p, int32_t v, uint32_t base, Work& wk, int lane) {
   const S* st = (const S*)p.st;
-  const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+  const int64_t beg = RP(p, v), end = RP(p, v + 1);
   for (;;) {
     uint32_t lo = 0, hi = 0;
     for (int64_t e = beg + lane; e < end; e += 32) {
@@ -378,7 +382,7 @@ __device__ __forceinline__ uint32_t firstfit_warp(const Params& p, int32_t v, ui
 template <class S, bool CW>
 __device__ __forceinline__ uint32_t firstfit_cta(const Params& p, int32_t v, uint32_t base, Work& wk, uint32_t* s_win) {
   const S* st = (const S*)p.st;
-  const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+  const int64_t beg = RP(p, v), end = RP(p, v + 1);
   for (;;) {
     if (threadIdx.x < 2) s_win[threadIdx.x] = 0;
     __syncthreads();
@@ -415,7 +419,7 @@ template <int POL>
 __device__ __forceinline__ bool recolors(const Params& p, int32_t v, int32_t w, int64_t dv) {
   if (POL == HIGHER_ID) return v > w;
   if (POL == LOWER_ID) return v < w;
-  const int64_t dw = ldr(p.rp, w + 1) - ldr(p.rp, w);
+  const int64_t dw = RP(p, w + 1) - RP(p, w);  // one partition only (DEGREE is single-GPU)
   return dv < dw || (dv == dw && v > w);
 }
 

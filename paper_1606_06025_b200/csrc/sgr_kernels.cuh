@@ -29,7 +29,7 @@ __device__ __forceinline__ void prologue_count(const Params& p) {
       const int64_t deg = ldr(p.rp, v + 1) - ldr(p.rp, v);
       if (sizeof(S) == 2 && deg > NARROW_MAX_DEG) wide = true;
       b = bin_of(p, deg);
-      sts(st + v, 1u);
+      sts(st + p.v_base + v, 1u);
       if (PUSH) {
         sts(p.fm + v, 0u);
         sts(p.fm2 + v, 0u);
@@ -61,7 +61,7 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
     int b = -1;
     WE e;
     if (act) {
-      e.v = (int32_t)v;
+      e.v = (int32_t)(p.v_base + v);
       e.k = -1;  // split computed by the first Phase B visit
       e.beg = ldr(p.rp, v);
       b = bin_of(p, ldr(p.rp, v + 1) - e.beg);
@@ -141,7 +141,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
       WE e;
       if (i < nb[0]) {
         e = ldw(Wb + i);
-        const int64_t deg = ldr(p.rp, e.v + 1) - e.beg;
+        const int64_t deg = RP(p, e.v + 1) - e.beg;
         if (deg <= 32) sts(st + e.v, firstfit_thread<S, CW>(p, e.v, 1u, wk));
         else big = true;
       }
@@ -229,7 +229,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
       if (i < cend) {
         e = ldw(Wb + i);
         tent = lds(st + e.v) & CM;
-        if (e.k < 0 || POL != HIGHER_ID) end = ldr(p.rp, e.v + 1);
+        if (e.k < 0 || POL != HIGHER_ID) end = RP(p, e.v + 1);
         if (e.k < 0 && POL != DEGREE) e.k = row_split(p, e.v, e.beg, end);
         const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
         lo = sr.lo;
@@ -293,7 +293,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
       if (state == 2) {
         sts(st + e.v, tent | SW<S>::COMMIT);
         if (PUSH && tent <= 64) {
-          if (end < 0) end = ldr(p.rp, e.v + 1);
+          if (end < 0) end = RP(p, e.v + 1);
           if (end - e.beg <= (int64_t)p.t1) scatter<1>(p, tent, e.beg, end);
           else big = true;
           if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
@@ -342,7 +342,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
     for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       WE e = ldw(Wb + i);
       const uint32_t tent = lds(st + e.v) & SW<S>::CMASK;
-      const int64_t end = ldr(p.rp, e.v + 1);
+      const int64_t end = RP(p, e.v + 1);
       if (e.k < 0 && POL != DEGREE) {
         if (threadIdx.x == 0) s_k = row_split(p, e.v, e.beg, end);
         __syncthreads();
@@ -386,7 +386,7 @@ __device__ __forceinline__ void epilogue(const Params& p) {
   uint32_t mx = 0;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < p.n; v += stride) {
-    const uint32_t c = lds(st + v) & SW<S>::CMASK;
+    const uint32_t c = lds(st + p.v_base + v) & SW<S>::CMASK;
     p.colors_out[v] = c;
     mx = c > mx ? c : mx;
   }
