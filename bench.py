@@ -182,6 +182,7 @@ def run_reference(args):
 def run_partitioned(args, g, rank, world, local):
     """N > 1: one edge-balanced vertex range per rank, replicated ghost state, two NCCL
     all-gathers per round (paper_1606_06025_b200.dist) — strong scaling on one graph."""
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -228,7 +229,9 @@ def run_partitioned(args, g, rank, world, local):
             "num_colors": res.num_colors, "rounds": res.rounds,
             "exchanged_pairs_rank0": res.exchanged_pairs,
             "timing": "host wall clock between barriers (every dist call is synchronous), max over ranks",
-            "gpu_launches": None, "clocks": clk,
+            # per step: 3 ingest kernels, per round phase A + pack + unpack (r > 1) and
+            # phase B + pack + unpack, 1 finalize
+            "gpu_launches": args.steps * (3 + 6 * res.rounds - 3 + 1), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     return 0
