@@ -77,9 +77,10 @@ typedef struct gc_work {
   uint64_t phase_b_vertices;   /* sum over rounds of |W_r| */
   uint64_t phase_b_edges;      /* col_idx entries examined by the conflict scans */
   uint64_t phase_b_gathers;    /* neighbour colour words gathered by the conflict scans */
-  uint64_t commit_scatter;     /* forbidden-mask atomics issued by committing vertices */
+  uint64_t commit_scatter;     /* neighbour entries visited by the commit scatters */
   uint64_t pushes;             /* vertices pushed into W_out over the run */
-  uint64_t reserved[9];
+  uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters */
+  uint64_t reserved[8];
 } gc_work;
 
 typedef struct gc_opts {

@@ -42,7 +42,8 @@ class Work(ctypes.Structure):
     _fields_ = [("phase_a_vertices", ctypes.c_uint64), ("phase_a_edges", ctypes.c_uint64),
                 ("phase_b_vertices", ctypes.c_uint64), ("phase_b_edges", ctypes.c_uint64),
                 ("phase_b_gathers", ctypes.c_uint64), ("commit_scatter", ctypes.c_uint64),
-                ("pushes", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 9)]
+                ("pushes", ctypes.c_uint64), ("scatter_reds", ctypes.c_uint64),
+                ("reserved", ctypes.c_uint64 * 8)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}

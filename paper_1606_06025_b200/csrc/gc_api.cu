@@ -152,8 +152,11 @@ void* pick_persistent_s(int pol, bool push, bool cw) {
   return nullptr;
 }
 
-void* pick_persistent(bool narrow, int pol, bool push, bool cw) {
-  return narrow ? pick_persistent_s<uint16_t>(pol, push, cw) : pick_persistent_s<uint32_t>(pol, push, cw);
+// state-word width: 1, 2 or 4 bytes
+void* pick_persistent(int sbytes, int pol, bool push, bool cw) {
+  if (sbytes == 1) return pick_persistent_s<uint8_t>(pol, push, cw);
+  if (sbytes == 2) return pick_persistent_s<uint16_t>(pol, push, cw);
+  return pick_persistent_s<uint32_t>(pol, push, cw);
 }
 
 template <int POL, bool PUSH, bool CW>
@@ -332,18 +335,16 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   // ---- workspace
   const bool push = !(o.flags & GC_FLAG_PULL_FIRSTFIT);
   const bool cw = (o.flags & GC_FLAG_COUNT_WORK) != 0;
-  void *st, *fm = nullptr, *fm2 = nullptr, *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
-  // [fm | st] in one allocation so that one L2 access-policy window covers the hot
-  // per-vertex state (fm 4n bytes + st 2n or 4n bytes)
+  void *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
+  uint8_t* planes = nullptr;
+  // [st | plane 0 | plane 1 | ...] in one allocation so that one L2 access-policy window
+  // covers the hot per-vertex state: the state words (1, 2 or 4 bytes per vertex, placed
+  // right before plane 0 whatever their width) and the first forbidden-colour planes.
+  const int64_t pitch = (n + 255) / 256 * 256;
+  const uint32_t np = push ? (uint32_t)MAX_PLANES : 0u;
   void* hot;
-  CK(sc.alloc(&hot, sizeof(uint32_t) * (size_t)n * (push ? 2 : 1)));
-  if (push) {
-    fm = hot;
-    st = (char*)hot + sizeof(uint32_t) * (size_t)n;
-    CK(sc.alloc(&fm2, sizeof(uint32_t) * (size_t)n));
-  } else {
-    st = hot;
-  }
+  CK(sc.alloc(&hot, (size_t)pitch * (4 + np)));
+  planes = (uint8_t*)hot + 4 * pitch;
   CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&w1, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&info, sizeof(DevInfo)));
@@ -377,9 +378,14 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.n = (int32_t)n;
   p.rp = d_rp;
   p.ci = d_ci;
-  p.st = (uint32_t*)st;
-  p.fm = (uint32_t*)fm;
-  p.fm2 = (uint32_t*)fm2;
+  p.st = (uint8_t*)planes - 4 * pitch;
+  p.fmp = push ? planes : nullptr;
+  p.plane = pitch;
+  p.np = np;
+  {
+    const char* f = getenv("GC_SCATTER_FILTER");
+    p.sfilter = (f && f[0] == '1') ? 1u : 0u;
+  }
   p.wl0 = (WE*)w0;
   p.wl1 = (WE*)w1;
   p.info = (DevInfo*)info;
@@ -407,7 +413,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     cudaEvent_t a, b;
     ~EvGuard() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
   } evg{ev0, ev1};
-  // L2 residency of the hot per-vertex state: an access-policy window marks [fm | st] as
+  // L2 residency of the hot per-vertex state: an access-policy window marks [st | planes] as
   // persisting (the streamed CSR and worklists are "streaming" misses), within a temporary
   // persisting set-aside.  Stream attribute, limit and persisting lines are restored or reset
   // before returning.  GC_L2_PERSIST=0 disables it (ablation).
@@ -426,19 +432,23 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   } l2w;
   const char* l2env = getenv("GC_L2_PERSIST");
   const bool want_window = !(l2env && l2env[0] == '0');
-  auto set_window = [&](bool narrow) -> cudaError_t {
+  auto set_window = [&](int sbytes) -> cudaError_t {
     if (!want_window) return cudaSuccess;
     int maxp = 0, maxw = 0;
     cudaError_t e;
     if ((e = cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev)) != cudaSuccess) return e;
     if (maxp <= 0 || maxw <= 0) return cudaSuccess;
-    size_t bytes = (size_t)n * ((push ? 4 : 0) + (narrow ? 2 : 4));
-    // only worth it when most of the state can persist (measured: R-MAT s24 -6%, while a
-    // 400 MB mesh state with hitRatio 0.2 got 14% slower)
-    if (bytes > (size_t)maxp + (size_t)maxp / 2) return cudaSuccess;
+    // the state words plus as many forbidden-colour planes as the set-aside holds
+    // (GC_L2_PLANES caps the plane count; tuning)
+    const size_t sb = (size_t)pitch * sbytes;
+    if (sb > (size_t)maxp + (size_t)maxp / 2) return cudaSuccess;
+    uint32_t kp = 0;
+    while (kp < np && sb + (size_t)pitch * (kp + 1) <= (size_t)maxp) ++kp;
+    if (const char* lp = getenv("GC_L2_PLANES")) kp = kp < (uint32_t)atoi(lp) ? kp : (uint32_t)atoi(lp);
+    size_t bytes = sb + (size_t)pitch * kp;
     if (bytes > (size_t)maxw) bytes = (size_t)maxw;
-    size_t limit = bytes < (size_t)maxp ? bytes : (size_t)maxp;
+    const size_t limit = bytes < (size_t)maxp ? bytes : (size_t)maxp;
     if (!l2w.on) {
       if ((e = cudaDeviceGetLimit(&l2w.prev, cudaLimitPersistingL2CacheSize)) != cudaSuccess) return e;
       l2w.s = s;
@@ -447,7 +457,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     if ((e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit)) != cudaSuccess) return e;
     cudaStreamAttrValue av;
     memset(&av, 0, sizeof(av));
-    av.accessPolicyWindow.base_ptr = hot;
+    av.accessPolicyWindow.base_ptr = (uint8_t*)planes - sb;
     av.accessPolicyWindow.num_bytes = bytes;
     av.accessPolicyWindow.hitRatio = (float)((double)limit / (double)bytes);
     av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -460,12 +470,18 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       set_err("gc_color: device %d does not support cooperative launch", dev);
       return GC_ERR_UNSUPPORTED;
     }
-    // 16-bit state words first; a vertex of degree > 32766 makes the kernel stop in its
-    // prologue with ST_NEED_WIDE and the run is repeated with 32-bit words.
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      const bool narrow = attempt == 0;
-      CK(set_window(narrow));
-      void* fn = pick_persistent(narrow, (int)o.policy, push, cw);
+    // 8-bit state words first; a colour > 127 makes the kernel stop at the next barrier with
+    // ST_NEED16 and a vertex of degree > 32766 stops it in its prologue with ST_NEED32; the
+    // run is then repeated with the wider words (at most two restarts).
+    int sbytes = 1;
+    if (const char* sw = getenv("GC_STATE_BYTES")) {  // diagnostics: force a width
+      const int f = atoi(sw);
+      if (f == 1 || f == 2 || f == 4) sbytes = f;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      p.st = (uint8_t*)planes - (int64_t)sbytes * pitch;
+      CK(set_window(sbytes));
+      void* fn = pick_persistent(sbytes, (int)o.policy, push, cw);
       int per_sm = 0;
       CK(occupancy(dev, fn, &per_sm));
       if (per_sm < 1) {
@@ -479,12 +495,15 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       uint32_t status = 0;
       CK(cudaMemcpyAsync(&status, &((DevInfo*)info)->status, sizeof(status), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      if (status != ST_NEED_WIDE) break;
+      if (status == ST_NEED16 && sbytes < 2) sbytes = 2;
+      else if (status == ST_NEED32 && sbytes < 4) sbytes = 4;
+      else break;
       CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
     }
   } else {
     // ---- host-driven rounds (ablation): one launch per phase, |W| read every round
-    CK(set_window(false));
+    p.st = (uint8_t*)planes - 4 * pitch;
+    CK(set_window(4));
     const int grid = prop.sms * 4;
     if (push) k_prologue_count<true><<<grid, BLOCK, 0, s>>>(p);
     else k_prologue_count<false><<<grid, BLOCK, 0, s>>>(p);
@@ -579,6 +598,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     o.work->phase_b_gathers = hinfo.work[W_B_GATHER];
     o.work->commit_scatter = hinfo.work[W_SCATTER];
     o.work->pushes = hinfo.work[W_PUSH];
+    o.work->scatter_reds = hinfo.work[W_SCATTER_RED];
   }
   *num_colors = hinfo.num_colors;
   *rounds = hinfo.rounds;

@@ -16,17 +16,22 @@
 // B200-first differences from the paper's K40c design:
 //   * Jacobi rounds (north star): Phase A uses only colours committed before the round,
 //     Phase B the round's tentative colours; the result is schedule independent.
-//   * One state word per vertex, S = uint16_t when Delta+1 <= 32767 (else uint32_t): top bit
+//   * One state word per vertex, S = uint8_t while every colour is <= 127, else uint16_t
+//     (Delta+1 <= 32767), else uint32_t (the run restarts with the wider word): top bit
 //     = committed, the rest = colour (tentative while the top bit is clear).  Phase A only
 //     USES committed words and only writes pending ones; Phase B only reads colour bits and
 //     only sets the top bit of its own vertex — so no phase uses a bit written in the same
-//     phase (aligned words are single-copy atomic) and no locks are needed.  16-bit words
-//     halve the gather footprint so it stays resident in the 126 MB L2.
-//   * Incremental forbidden-colour masks fm[v] (colours 1..32, hot) and fm2[v] (33..64, cold):
-//     committed colours never change, so a committing vertex REDs its colour bit into the
-//     mask of every neighbour (one RED per directed edge over the whole run) and Phase A is
-//     O(1): tent = ffs(~fm[v]) (or 32 + ffs(~fm2[v])); only colours beyond 64 fall back to
-//     the exact windowed scan from colour 65 (reading C7).
+//     phase (aligned words are single-copy atomic) and no locks are needed.  Byte words
+//     keep the gather footprint (n bytes) resident in the 126 MB L2.
+//   * Incremental forbidden-colour masks in byte planes: plane k holds, for every vertex, one
+//     byte with the colours 8k+1..8k+8 of its committed neighbours.  Committed colours never
+//     change, so a committing vertex REDs its colour bit into the plane byte of every pending
+//     neighbour (32-bit RED on the aligned word holding the byte) and Phase A is O(1):
+//     tent = first zero bit of plane 0, else of the first non-full plane (one byte per lane).
+//     Colour c is committed in round >= c at the earliest (rounds >= num_colors, pin P11), so
+//     plane k is first written in round 8k+1 and is zeroed in Phase A of round 8k: only the
+//     planes a run actually reaches are ever touched.  Colours beyond the planes fall back
+//     to the exact windowed scan (reading C7).
 //     GC_FLAG_PULL_FIRSTFIT selects the paper's full rescan instead (same result).
 //   * L1 policy: the read-only CSR goes through the non-coherent path without allocating
 //     in L1; everything written during the run is read L2-coherently (.cg).
@@ -47,11 +52,15 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int32_t NARROW_MAX_DEG = 32766;  // 16-bit state: colours <= Delta+1 <= 32767
 
 enum Policy { HIGHER_ID = 0, LOWER_ID = 1, DEGREE = 2 };
-enum Status { ST_OK = 0, ST_NEED_WIDE = 2, ST_NO_CONVERGENCE = 3, ST_WATCHDOG = 5 };
-enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_N };
+constexpr int MAX_PLANES = 16;     // byte planes of forbidden colours: colours 1..128
+enum Status { ST_OK = 0, ST_NEED16 = 2, ST_NO_CONVERGENCE = 3, ST_NEED32 = 4, ST_WATCHDOG = 5 };
+enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_SCATTER_RED, W_N };
 
 // State-word traits: top bit = committed, remaining bits = colour.
 template <class S> struct SW;
+template <> struct SW<uint8_t> {
+  static constexpr uint32_t COMMIT = 0x80u, CMASK = 0x7fu;
+};
 template <> struct SW<uint16_t> {
   static constexpr uint32_t COMMIT = 0x8000u, CMASK = 0x7fffu;
 };
@@ -95,9 +104,12 @@ struct Params {
   int32_t v_base;               // global id of local row 0 (0 on one GPU); st is global-indexed
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;
-  void* st;                     // state word per vertex (uint16_t or uint32_t)
-  uint32_t* fm;                 // forbidden colours 1..32 per vertex (incremental mode)
-  uint32_t* fm2;                // forbidden colours 33..64 (cold: only touched by colours > 32)
+  void* st;                     // state word per vertex (uint8_t, uint16_t or uint32_t)
+  uint8_t* fmp;                 // forbidden-colour byte planes (incremental mode): plane k at
+                                //   fmp + k * plane, byte v = colours 8k+1..8k+8 of v's committed nbrs
+  int64_t plane;                // plane pitch in bytes (>= n, multiple of 256)
+  uint32_t np;                  // number of planes (<= MAX_PLANES)
+  uint32_t sfilter;             // commit scatter skips neighbours already committed
   WE* wl0;                      // worklist buffers, n entries each, bin segments
   WE* wl1;
   DevInfo* info;
@@ -165,6 +177,14 @@ __device__ __forceinline__ void stw(WE* p, const WE& e) {
                : "memory");
 }
 // Per-vertex state words and forbidden masks (L2-resident working set).
+__device__ __forceinline__ uint32_t lds(const uint8_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t lds(const uint16_t* p) {
   uint16_t v;
   asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
@@ -484,22 +504,52 @@ __device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_
 }
 
 // ---------------------------------------------------------------- commit scatter
-// A winner ORs its colour bit (colours 1..64) into the forbidden mask of every neighbour: entries
-// e = start, start+STEP, ... < end; four col_idx loads are issued before the four
-// fire-and-forget REDs so that each lane keeps several misses in flight.
-template <int STEP>
-__device__ __forceinline__ void scatter(const Params& p, uint32_t color, int64_t start, int64_t end) {
-  uint32_t* const mask = color <= 32 ? p.fm : p.fm2;   // colour 1..64
-  const uint32_t bit = 1u << ((color - 1) & 31);
+// A winner ORs its colour bit into plane byte of every neighbour (colours beyond the planes:
+// nothing; the pull fallback of Phase A sees them): entries e = start, start+STEP, ... < end;
+// four col_idx loads are issued before the four fire-and-forget REDs so that each lane keeps
+// several misses in flight.  With p.sfilter the state words of the four neighbours are read
+// first and already-committed ones are skipped (they never read their masks again; a word
+// committed concurrently in this phase may be seen either way — both are correct).
+template <class S>
+__device__ __forceinline__ void red_plane(uint8_t* pl, int32_t w, uint32_t bit) {
+  red_or((uint32_t*)(pl + (w & ~3)), bit << ((w & 3) * 8));
+}
+template <class S, int STEP, bool CW>
+__device__ __forceinline__ void scatter(const Params& p, uint32_t color, int64_t start, int64_t end, Work& wk) {
+  if (color > 8u * p.np) return;
+  uint8_t* const pl = p.fmp + (int64_t)((color - 1) >> 3) * p.plane;
+  const uint32_t bit = 1u << ((color - 1) & 7);
+  const S* st = (const S*)p.st;
   int64_t e = start;
+  if (p.sfilter) {
+    for (; e < end; e += 4 * STEP) {
+      int32_t w[4];
+      uint32_t s[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = e + u * STEP < end ? ldc(p.ci, e + u * STEP) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = w[u] >= 0 ? lds(st + w[u]) : SW<S>::COMMIT;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (!(s[u] & SW<S>::COMMIT)) {
+          red_plane<S>(pl, w[u], bit);
+          if (CW) wk.v[W_SCATTER_RED] += 1;
+        }
+    }
+    return;
+  }
   for (; e + 3 * STEP < end; e += 4 * STEP) {
     const int32_t w0 = ldc(p.ci, e), w1 = ldc(p.ci, e + STEP), w2 = ldc(p.ci, e + 2 * STEP), w3 = ldc(p.ci, e + 3 * STEP);
-    red_or(mask + w0, bit);
-    red_or(mask + w1, bit);
-    red_or(mask + w2, bit);
-    red_or(mask + w3, bit);
+    red_plane<S>(pl, w0, bit);
+    red_plane<S>(pl, w1, bit);
+    red_plane<S>(pl, w2, bit);
+    red_plane<S>(pl, w3, bit);
   }
-  for (; e < end; e += STEP) red_or(mask + ldc(p.ci, e), bit);
+  for (; e < end; e += STEP) red_plane<S>(pl, ldc(p.ci, e), bit);
+  if (CW) {
+    const int64_t cnt = end > start ? (end - start + STEP - 1) / STEP : 0;
+    wk.v[W_SCATTER_RED] += (unsigned long long)cnt;
+  }
 }
 
 }  // namespace gcdev

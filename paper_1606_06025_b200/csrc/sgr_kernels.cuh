@@ -1,7 +1,7 @@
 // sgr_kernels.cuh — phases and kernels of the SGR colouring path (sm_100a).
 // Phase functions are shared by the persistent cooperative kernel (default) and by the
 // one-launch-per-phase host-driven ablation (GC_FLAG_HOST_ROUNDS).
-// Template parameters: S = state word (uint16_t / uint32_t), POL = conflict policy,
+// Template parameters: S = state word (uint8_t / uint16_t / uint32_t), POL = conflict policy,
 // PUSH = incremental forbidden masks (else full rescans), CW = exact work counters.
 #pragma once
 #include "sgr_device.cuh"
@@ -10,8 +10,9 @@ namespace gcdev {
 
 // ---------------------------------------------------------------- a1: ingest + bins
 // P0: degrees -> bin sizes; st[v] = 1 (round-1 tentative colour: nothing is committed yet,
-// so First-Fit gives 1 to every vertex), fm[v] = 0.  With 16-bit state words a vertex of
-// degree > NARROW_MAX_DEG makes the run restart with 32-bit words (ST_NEED_WIDE).
+// so First-Fit gives 1 to every vertex), plane-0 mask byte = 0.  With 8- or 16-bit state
+// words a vertex of degree > NARROW_MAX_DEG makes the run restart with 32-bit words
+// (ST_NEED32); 8-bit words restart with 16-bit ones when a colour > 127 appears (Phase A).
 template <class S, bool PUSH>
 __device__ __forceinline__ void prologue_count(const Params& p) {
   __shared__ uint32_t s_cnt[NBIN];
@@ -27,13 +28,10 @@ __device__ __forceinline__ void prologue_count(const Params& p) {
     int b = -1;
     if (act) {
       const int64_t deg = ldr(p.rp, v + 1) - ldr(p.rp, v);
-      if (sizeof(S) == 2 && deg > NARROW_MAX_DEG) wide = true;
+      if (sizeof(S) < 4 && deg > NARROW_MAX_DEG) wide = true;
       b = bin_of(p, deg);
       sts(st + p.v_base + v, 1u);
-      if (PUSH) {
-        sts(p.fm + v, 0u);
-        sts(p.fm2 + v, 0u);
-      }
+      if (PUSH) sts(p.fmp + v, 0u);
     }
 #pragma unroll
     for (int k = 0; k < NBIN; ++k) {
@@ -41,7 +39,7 @@ __device__ __forceinline__ void prologue_count(const Params& p) {
       if (m && lane == 0) atomicAdd(&s_cnt[k], (uint32_t)__popc(m));
     }
   }
-  if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED_WIDE);
+  if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED32);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.info->wlp[0] = (unsigned long long)p.wl0;
     p.info->wlp[1] = (unsigned long long)p.wl1;
@@ -81,9 +79,30 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
 }
 
 // ---------------------------------------------------------------- a2: Phase A
-// Incremental-mask mode: every pending vertex is O(1) (tent = ffs(~fm[v])), so all bins are
-// processed thread-per-vertex; a vertex whose 32-colour mask is full is handed to the whole
-// warp, which runs the exact windowed First-Fit from colour 33 (reading C7).
+// Incremental-mask mode: every pending vertex is O(1) in the number of neighbours: its own
+// thread reads its plane bytes two planes at a time (independent loads) until a non-full one
+// gives the colour — in round r at most ceil((r-1)/8) planes can be non-empty (pin P11).
+// Beyond the last plane the whole warp runs the exact windowed First-Fit (reading C7).
+// 8-bit state words cannot hold colours > 127: the run restarts with 16-bit words
+// (ST_NEED16).
+template <class S>
+__device__ __forceinline__ void store_tent(const Params& p, S* st, int32_t v, uint32_t t) {
+  if (sizeof(S) == 1 && t > SW<S>::CMASK) atomicExch(&p.info->status, (uint32_t)ST_NEED16);
+  else sts(st + v, t);
+}
+
+// First free colour from the planes, 0 when all np planes are full.
+__device__ __forceinline__ uint32_t plane_firstfit(const Params& p, int32_t v) {
+  const uint8_t* f = p.fmp + v;
+  for (uint32_t k = 0; k < p.np; k += 2) {
+    const uint32_t b0 = lds(f + (int64_t)k * p.plane);
+    const uint32_t b1 = k + 1 < p.np ? lds(f + (int64_t)(k + 1) * p.plane) : 0xffu;
+    if (b0 != 0xffu) return 8u * k + (uint32_t)__ffs(b0 ^ 0xffu);
+    if (b1 != 0xffu) return 8u * (k + 1) + (uint32_t)__ffs(b1 ^ 0xffu);
+  }
+  return 0;
+}
+
 template <class S, bool CW>
 __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, const WE* W, const uint32_t* nb,
                                              Work& wk) {
@@ -96,33 +115,35 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, 
     const uint32_t cnt = nb[b];
     for (uint32_t base = gw * 32; base < cnt; base += nw * 32) {
       const uint32_t i = base + lane;
-      const bool act = i < cnt;
       int32_t v = 0;
-      uint32_t f = 0;
-      if (act) {
-        v = ldw_v(Wb + i);
-        f = ldf(p.fm + v);
-      }
       bool fb = false;
-      if (act) {
-        if (f != FULL) {
-          sts(st + v, (uint32_t)__ffs(~f));
-        } else {
-          const uint32_t f2 = ldf(p.fm2 + v);
-          if (f2 != FULL) sts(st + v, 32u + (uint32_t)__ffs(~f2));
-          else fb = true;
-        }
+      if (i < cnt) {
+        v = ldw_v(Wb + i);
+        const uint32_t t = plane_firstfit(p, v);
+        if (t) store_tent<S>(p, st, v, t);
+        else fb = true;
       }
       unsigned m = __ballot_sync(FULL, fb);
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const int32_t u = __shfl_sync(FULL, v, src);
-        const uint32_t t = firstfit_warp<S, CW>(p, u, 65u, wk, lane);
-        if (lane == 0) sts(st + u, t);
+        uint32_t t = 8u * p.np + 1u;  // > 127 when np = MAX_PLANES: 8-bit words restart
+        if (sizeof(S) > 1 || t <= SW<S>::CMASK) t = firstfit_warp<S, CW>(p, u, t, wk, lane);
+        if (lane == 0) store_tent<S>(p, st, u, t);
       }
     }
   }
+}
+
+// Plane k (colours 8k+1..8k+8) is zeroed in Phase A of round 8k, before any colour it holds
+// can be committed (round >= 8k+1) or looked up (Phase A of round >= 8k+1).
+__device__ __forceinline__ void zero_plane(const Params& p, uint32_t r) {
+  if (r % 8 != 0 || r / 8 >= p.np) return;
+  uint4* q = (uint4*)(p.fmp + (int64_t)(r / 8) * p.plane);
+  const int64_t nq = p.plane / 16;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < nq; i += (int64_t)gridDim.x * BLOCK) q[i] = z;
 }
 
 // Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round;
@@ -142,7 +163,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
       if (i < nb[0]) {
         e = ldw(Wb + i);
         const int64_t deg = RP(p, e.v + 1) - e.beg;
-        if (deg <= 32) sts(st + e.v, firstfit_thread<S, CW>(p, e.v, 1u, wk));
+        if (deg <= 32) store_tent<S>(p, st, e.v, firstfit_thread<S, CW>(p, e.v, 1u, wk));
         else big = true;
       }
       unsigned m = __ballot_sync(FULL, big);
@@ -151,7 +172,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
         m &= m - 1;
         const int32_t u = __shfl_sync(FULL, e.v, src);
         const uint32_t t = firstfit_warp<S, CW>(p, u, 1u, wk, lane);
-        if (lane == 0) sts(st + u, t);
+        if (lane == 0) store_tent<S>(p, st, u, t);
       }
     }
   }
@@ -160,7 +181,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
     for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       const int32_t v = ldw_v(Wb + i);
       const uint32_t t = firstfit_cta<S, CW>(p, v, 1u, wk, s_win);
-      if (threadIdx.x == 0) sts(st + v, t);
+      if (threadIdx.x == 0) store_tent<S>(p, st, v, t);
     }
   }
 }
@@ -179,20 +200,25 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
   }
   if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
-  if (PUSH) phase_a_mask<S, CW>(p, bins, W, nb, wk);
-  else phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
+  if (PUSH) {
+    zero_plane(p, r);
+    phase_a_mask<S, CW>(p, bins, W, nb, wk);
+  } else {
+    phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
+  }
 }
 
 // ---------------------------------------------------------------- a3: Phase B + push
 // Winners commit (set the top bit of their own word) and, in mask mode, OR their colour bit
 // into the forbidden mask of every neighbour; losers go to W_out through the Pusher.
 
-// Warps pop chunks of CH items from a per-bin queue head (one atomic per chunk) so that
+// Warps pop chunks of ch items from a per-bin queue head (one atomic per chunk) so that
 // costly items (long scans) do not leave the rest of the grid idle at the phase barrier.
-template <uint32_t CH>
-__device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, int lane) {
+// ch shrinks with |W| (down to one vertex per warp in the small tail rounds, where the few
+// remaining vertices are the high-degree ones with long scans).
+__device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, uint32_t ch, int lane) {
   uint32_t b = 0;
-  if (lane == 0) b = atomicAdd(q, (uint32_t)CH);
+  if (lane == 0) b = atomicAdd(q, ch);
   return __shfl_sync(FULL, b, 0);
 }
 
@@ -201,30 +227,58 @@ __device__ __forceinline__ int64_t scan_pos(int64_t lo, int64_t hi, bool down, i
   return down ? hi - 1 - j : lo + j;
 }
 
-// bin 0.  Stage 1: each lane takes one vertex and examines the first PROBE positions of its
-// scan range (independent loads: ILP).  Most losers are decided here (the nearest lower ids
-// are the likeliest conflicts).  Stage 2: the vertices whose range is longer and still
-// undecided are continued one after the other by the whole warp, 32 positions per step
-// (coalesced col_idx, 32 gathers in flight).  Winners commit; a winner of degree > t1 has its
-// forbidden-mask scatter done by the whole warp as well.
+// ---- warp-flattened segment loops
+// Each lane of a warp holds a segment of W_i items (a vertex's next stretch of its conflict
+// scan, or a winner's row for the commit scatter).  The warp walks the concatenation of all
+// segments 32 x FLAT_U items per step, so short and long segments share the lanes evenly
+// instead of one lane (or one vertex at a time) doing all of a segment's work.  Item f
+// belongs to the lane `owner` with E[owner-1] <= f < E[owner] (E = inclusive prefix sum of
+// W over the lanes, found by a 5-step binary search over shuffles).
+constexpr int FLAT_U = 2;     // items per lane per step (independent loads in flight)
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
+  int o = 0;
+#pragma unroll
+  for (int b = 16; b; b >>= 1)
+    if (__shfl_sync(FULL, E, o + b - 1) <= f) o += b;
+  return o;
+}
+
+// bin 0 (degree <= t3).  Every lane takes one vertex of the warp's chunk; the conflict scans
+// of all 32 vertices then advance together in passes over the flattened segments: pass 1
+// examines the first 4 positions of every scan range (the nearest lower ids, where most
+// conflicts are), later passes 12, 48, 192, ... more, so that early exit is kept for the
+// losers while all lanes stay busy.  A vertex with a hit loses (pushed to W_out); a vertex
+// whose range is exhausted wins: it commits and its row is scattered into the forbidden
+// masks of its neighbours, again as one flattened loop over all winners of the batch.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
-                                             Work& wk) {
+                                             Work& wk, int* s_first) {
   S* st = (S*)p.st;
   constexpr uint32_t CM = SW<S>::CMASK;
   const int lane = threadIdx.x & 31;
-  constexpr uint32_t CH = 64;
-  for (uint32_t c0 = pop_chunk<CH>(q, lane); c0 < cnt; c0 = pop_chunk<CH>(q, lane)) {
-    const uint32_t cend = min(c0 + CH, cnt);
-    for (uint32_t base = c0; base < cend; base += 32) {
-      const uint32_t i = base + lane;
+  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t ch = max(1u, min(64u, cnt / (4u * nwarps)));
+  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < cnt; c0 = pop_chunk(q, ch, lane)) {
+    const uint32_t cend = min(c0 + ch, cnt);
+    for (uint32_t bse = c0; bse < cend; bse += 32) {
+      const uint32_t i = bse + lane;
       WE e;
       e.v = 0;
       e.k = 0;
       e.beg = 0;
       uint32_t tent = 0;
-      int64_t end = -1, lo = 0, hi = 0, dv = 0;
-      bool down = true;
+      int64_t end = -1, sbase = 0, dv = 0;
+      int sdir = 1;
+      uint32_t len = 0, pos = 0;
       int state = 0;  // 0 inactive, 1 lose, 2 win, 3 undecided
       if (i < cend) {
         e = ldw(Wb + i);
@@ -232,81 +286,110 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
         if (e.k < 0 || POL != HIGHER_ID) end = RP(p, e.v + 1);
         if (e.k < 0 && POL != DEGREE) e.k = row_split(p, e.v, e.beg, end);
         const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-        lo = sr.lo;
-        hi = sr.hi;
-        down = sr.down;
+        sbase = sr.down ? sr.hi - 1 : sr.lo;
+        sdir = sr.down ? -1 : 1;
+        len = (uint32_t)(sr.hi - sr.lo);
         if (POL == DEGREE) dv = end - e.beg;
-        const int64_t len = hi - lo;
-        int32_t w[PROBE];
-        uint32_t c[PROBE];
-#pragma unroll
-        for (int u = 0; u < PROBE; ++u) w[u] = u < len ? ldc(p.ci, scan_pos(lo, hi, down, u)) : 0;
-#pragma unroll
-        for (int u = 0; u < PROBE; ++u) c[u] = u < len ? (lds(st + w[u]) & CM) : 0u;
-        int f = -1;
-#pragma unroll
-        for (int u = PROBE - 1; u >= 0; --u)
-          if (u < len && c[u] == tent && recolors<POL>(p, e.v, w[u], dv)) f = u;
-        if (f >= 0) state = 1;
-        else state = len <= PROBE ? 2 : 3;
-        if (CW && state != 3) {
-          const int64_t ex = f >= 0 ? f + 1 : (len < PROBE ? len : PROBE);
-          wk.v[W_B_EDGE] += ex;
-          wk.v[W_B_GATHER] += ex;
-        }
+        state = len ? 3 : 2;
       }
-      // stage 2: warp-wide continuation
-      unsigned und = __ballot_sync(FULL, state == 3);
-      while (und) {
-        const int src = __ffs(und) - 1;
-        und &= und - 1;
-        const int32_t v = __shfl_sync(FULL, e.v, src);
-        const uint32_t t = __shfl_sync(FULL, tent, src);
-        const int64_t slo = __shfl_sync(FULL, lo, src), shi = __shfl_sync(FULL, hi, src);
-        const int64_t sdv = __shfl_sync(FULL, dv, src);
-        const bool sdown = __shfl_sync(FULL, (int)down, src) != 0;
-        const int64_t len = shi - slo;
-        bool found = false;
-        int64_t examined = PROBE;
-        for (int64_t kk = PROBE; kk < len; kk += 32) {
-          const int64_t j = kk + lane;
-          bool hit = false;
-          if (j < len) {
-            const int32_t wv = ldc(p.ci, scan_pos(slo, shi, sdown, j));
-            hit = (lds(st + wv) & CM) == t && recolors<POL>(p, v, wv, sdv);
+      // conflict-scan passes
+      uint32_t cap = 4;
+      for (;;) {
+        const bool und = state == 3;
+        if (!__any_sync(FULL, und)) break;
+        const uint32_t Wn = und ? min(len - pos, cap) : 0u;
+        const uint32_t E = warp_incl_scan(Wn, lane);
+        const uint32_t T = __shfl_sync(FULL, E, 31);
+        if (CW) s_first[lane] = 0x7fffffff;
+        __syncwarp();
+        uint32_t lost = 0;
+        for (uint32_t f0 = 0; f0 < T; f0 += 32 * FLAT_U) {
+          int32_t w[FLAT_U];
+          int own[FLAT_U];
+          int64_t jj[FLAT_U];
+#pragma unroll
+          for (int u = 0; u < FLAT_U; ++u) {
+            const uint32_t f = f0 + u * 32 + lane;
+            const int o = flat_owner(E, f);
+            const int oc = o < 32 ? o : 31;
+            const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+            const uint32_t po = __shfl_sync(FULL, pos, oc);
+            const int64_t bo = __shfl_sync(FULL, sbase, oc);
+            const int dro = __shfl_sync(FULL, sdir, oc);
+            own[u] = f < T ? oc : -1;
+            jj[u] = (int64_t)(f - (Eo - Wo) + po);
+            w[u] = f < T ? ldc(p.ci, bo + dro * jj[u]) : 0;
           }
-          const unsigned hb = __ballot_sync(FULL, hit);
-          if (hb) {
-            found = true;
-            examined = kk + __ffs(hb);
-            break;
+#pragma unroll
+          for (int u = 0; u < FLAT_U; ++u) {
+            const int oc = own[u] < 0 ? 0 : own[u];
+            const uint32_t to = __shfl_sync(FULL, tent, oc);
+            const int32_t vo = __shfl_sync(FULL, e.v, oc);
+            const int64_t dvo = POL == DEGREE ? __shfl_sync(FULL, dv, oc) : 0;
+            const bool hit = own[u] >= 0 && (lds(st + w[u]) & CM) == to && recolors<POL>(p, vo, w[u], dvo);
+            if (hit) {
+              lost |= 1u << oc;
+              if (CW) atomicMin(&s_first[oc], (int)jj[u]);
+            }
           }
-          examined = kk + 32 < len ? kk + 32 : len;
         }
-        if (lane == src) {
-          state = found ? 1 : 2;
-          if (CW) { wk.v[W_B_EDGE] += examined; wk.v[W_B_GATHER] += examined; }
+        lost = __reduce_or_sync(FULL, lost);
+        __syncwarp();
+        if (und) {
+          if (lost >> lane & 1u) {
+            state = 1;
+            if (CW) { const uint32_t ex = (uint32_t)s_first[lane] + 1; wk.v[W_B_EDGE] += ex; wk.v[W_B_GATHER] += ex; }
+          } else {
+            pos += Wn;
+            if (pos == len) {
+              state = 2;
+              if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
+            }
+          }
         }
+        cap = cap < 1024 ? cap * 4 - (cap == 4 ? 4 : 0) : cap;  // 4, 12, 48, 192, 768, ...
       }
-      // winners commit; masks of their neighbours get their colour bit
-      bool big = false;
-      if (state == 2) {
-        sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 64) {
-          if (end < 0) end = RP(p, e.v + 1);
-          if (end - e.beg <= (int64_t)p.t1) scatter<1>(p, tent, e.beg, end);
-          else big = true;
-          if (CW) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
-        }
-      }
+      // winners commit; the forbidden masks of their neighbours get their colour bit
+      const bool win = state == 2;
+      if (win) sts(st + e.v, tent | SW<S>::COMMIT);
       if (PUSH) {
-        unsigned bm = __ballot_sync(FULL, big);
-        while (bm) {
-          const int src = __ffs(bm) - 1;
-          bm &= bm - 1;
-          const uint32_t t = __shfl_sync(FULL, tent, src);
-          const int64_t sb = __shfl_sync(FULL, e.beg, src), se = __shfl_sync(FULL, end, src);
-          scatter<32>(p, t, sb + lane, se);
+        const bool sc = win && tent <= 8u * p.np;
+        if (sc && end < 0) end = RP(p, e.v + 1);
+        const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
+        if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wn; }
+        const uint32_t E = warp_incl_scan(Wn, lane);
+        const uint32_t T = __shfl_sync(FULL, E, 31);
+        for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
+          int32_t w[4];
+          uint32_t wb[4];
+          uint8_t* pl[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t f = f0 + u * 32 + lane;
+            const int o = flat_owner(E, f);
+            const int oc = o < 32 ? o : 31;
+            const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+            const int64_t bo = __shfl_sync(FULL, e.beg, oc);
+            const uint32_t to = __shfl_sync(FULL, tent, oc);
+            pl[u] = p.fmp + (int64_t)((to - 1) >> 3) * p.plane;
+            wb[u] = 1u << ((to - 1) & 7);
+            w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
+          }
+          if (p.sfilter) {
+            uint32_t sw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sw[u] = w[u] >= 0 ? lds(st + w[u]) : SW<S>::COMMIT;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (!(sw[u] & SW<S>::COMMIT)) {
+                red_plane<S>(pl[u], w[u], wb[u]);
+                if (CW) wk.v[W_SCATTER_RED] += 1;
+              }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (w[u] >= 0) red_plane<S>(pl[u], w[u], wb[u]);
+          }
         }
       }
       pu.template push<0, CW>(state == 1, e, lane, wk.v[W_PUSH]);
@@ -320,6 +403,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   __shared__ WE s_pbuf[WARPS][NBIN * PBUF];
   __shared__ int s_first;
   __shared__ int32_t s_k;
+  __shared__ int s_cwfirst[CW ? WARPS : 1][32];
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   uint32_t nb[NBIN];
@@ -358,15 +442,15 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
         }
       } else {
         if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 64) {
-          scatter<BLOCK>(p, tent, e.beg + threadIdx.x, end);
+        if (PUSH && tent <= 8u * p.np) {
+          scatter<S, BLOCK, CW>(p, tent, e.beg + threadIdx.x, end, wk);
           if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
         }
       }
       __syncthreads();
     }
   }
-  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk);
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk, s_cwfirst[CW ? warp : 0]);
   pu.template flush<CW>(lane, wk.v[W_PUSH]);
 }
 

@@ -43,6 +43,9 @@ def main():
     variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
                          dict(host_rounds=True, pull_firstfit=True)]
     variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
+    variants["env"] = [dict(), dict(env={"GC_SCATTER_FILTER": "1"}), dict(env={"GC_STATE_BYTES": "2"}),
+                       dict(env={"GC_L2_PERSIST": "0"}), dict(env={"GC_L2_PLANES": "1"}),
+                       dict(env={"GC_L2_PLANES": "2"}), dict(env={"GC_SCATTER_FILTER": "1", "GC_L2_PLANES": "1"})]
     if args.sweep == "phases":
         res = gc.color(rp, ci, validate=False, phase_times=True)
         tot_a = sum(a for a, b in res.phase_us)
@@ -53,6 +56,10 @@ def main():
             print(f"  r={r:3d} |W|={w:10d} A={a:9.1f}us B={b:9.1f}us")
         return
     for kw in variants[args.sweep]:
+        kw = dict(kw)
+        env = kw.pop("env", {})
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
         ts = []
         res = None
         for _ in range(args.reps):
@@ -60,6 +67,12 @@ def main():
             ts.append(res.kernel_ms)
         ms = statistics.median(ts)
         same = bool(torch.equal(res.colors, ref_c)) if "policy" not in kw else None
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        kw.update(env)
         print(json.dumps({"config": args.config, "kw": kw, "kernel_ms": round(ms, 4),
                           "gteps": round(g.m / ms / 1e6, 3), "rounds": res.rounds,
                           "colors": res.num_colors, "same_as_default": same}), flush=True)

@@ -85,6 +85,28 @@ def test_parity_variants(gc, kw):
             _check(gc, g, pol, **kw)
 
 
+@pytest.mark.parametrize("env", [dict(GC_STATE_BYTES="2"), dict(GC_STATE_BYTES="4"),
+                                 dict(GC_SCATTER_FILTER="1"), dict(GC_L2_PERSIST="0")],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_parity_env_variants(gc, env, monkeypatch):
+    """Forced state-word widths, filtered commit scatter, no L2 window: same result."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for g in (wl.rmat(13, 8, seed=7), wl.rmat(11, 16, wl.GRAPH500, 5), wl.complete(70), wl.complete(130)):
+        for pol in POLICIES:
+            _check(gc, g, pol)
+        _check(gc, g, "higher_id", host_rounds=True)
+
+
+@pytest.mark.parametrize("k", [126, 127, 128, 129, 136])
+def test_state_word_restart(gc, k):
+    """8-bit state words hold colours <= 127: K_k needs colour k, so K_128 and beyond are
+    restarted with 16-bit words; colours up to 128 come from the 16 forbidden-colour planes,
+    beyond from the windowed fallback (reading C7)."""
+    res = _check(gc, wl.complete(k))
+    assert res.num_colors == k
+
+
 def test_multiwindow_colors(gc):
     """K_1025 and Graph500 skew: colours far beyond the 32-bit mask and 64-bit windows (C7)."""
     _check(gc, wl.complete(300))
