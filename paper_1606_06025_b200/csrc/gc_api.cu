@@ -345,6 +345,21 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   void* hot;
   CK(sc.alloc(&hot, (size_t)pitch * (4 + np)));
   planes = (uint8_t*)hot + 4 * pitch;
+  // dense rounds (push mode, persistent driver): per-vertex split + static heavy-vertex list
+  uint32_t dense_div = 4;  // sweep (R-MAT s24, stencil 128^3, mesh 8192^2): 2..64 -> 4
+  if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
+  if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
+  const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 512;
+  void *ksplit = nullptr, *heavy = nullptr;
+  if (dense_div) {
+    if (m < 0) {
+      CK(cudaMemcpyAsync(&m, d_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    const int64_t hcap = m / ((int64_t)t3 + 1) + 1;  // vertices of degree > t3
+    CK(sc.alloc(&ksplit, sizeof(int32_t) * (size_t)n));
+    CK(sc.alloc(&heavy, sizeof(WE) * (size_t)(hcap < n ? hcap : n)));
+  }
   CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&w1, sizeof(WE) * (size_t)n));
   CK(sc.alloc(&info, sizeof(DevInfo)));
@@ -400,7 +415,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.colors_out = (uint32_t*)dcol;
   p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
   p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
-  p.t3 = o.warp_bin_max ? o.warp_bin_max : 512;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
+  p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
+  p.dense_div = dense_div;
+  p.ksplit = (int32_t*)ksplit;
+  p.heavy = (WE*)heavy;
   p.timeout_ns = 60ull * 1000000000ull;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -110,6 +110,9 @@ struct Params {
   int64_t plane;                // plane pitch in bytes (>= n, multiple of 256)
   uint32_t np;                  // number of planes (<= MAX_PLANES)
   uint32_t sfilter;             // commit scatter skips neighbours already committed
+  uint32_t dense_div;           // dense rounds while |W_r| * dense_div > n (0: always sparse)
+  int32_t* ksplit;              // dense mode: number of lower-id neighbours of every vertex
+  WE* heavy;                    // dense mode: the vertices of degree > t3 {v, split, row start}
   WE* wl0;                      // worklist buffers, n entries each, bin segments
   WE* wl1;
   DevInfo* info;
@@ -201,6 +204,11 @@ __device__ __forceinline__ void sts(uint16_t* p, uint32_t v) {
 __device__ __forceinline__ void sts(uint32_t* p, uint32_t v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int32_t ldks(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ldf(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -276,12 +284,14 @@ __device__ __forceinline__ int bin_of(const Params& p, int64_t deg) { return deg
 // Offsets of the bin segments inside each worklist buffer (fixed for the whole run).
 struct Bins {
   uint32_t off[NBIN];
+  uint32_t size[NBIN];
   __device__ __forceinline__ void load(const Params& p) {
     uint32_t acc = 0;
 #pragma unroll
     for (int b = 0; b < NBIN; ++b) {
       off[b] = acc;
-      acc += ld_relaxed(&p.info->binsize[b]);
+      size[b] = ld_relaxed(&p.info->binsize[b]);
+      acc += size[b];
     }
   }
 };
@@ -291,7 +301,7 @@ struct Bins {
 // with ONE global atomic per 32 pushes (coalesced 128-B stores); remainders are flushed at
 // the end of the phase.  Counts are warp-uniform registers.
 struct Pusher {
-  WE* buf;                 // this warp's [NBIN][PBUF] staging area (shared memory)
+  WE* buf;                 // this warp's [PBUF] staging area (shared memory; bin 0 only)
   WE* out;                 // W_out
   uint32_t* gcnt;          // &info->cnt[next][0]
   uint32_t off[NBIN];
@@ -307,7 +317,8 @@ struct Pusher {
   __device__ __forceinline__ void push(bool pred, const WE& v, int lane, unsigned long long& pushed) {
     const unsigned m = __ballot_sync(FULL, pred);
     if (!m) return;
-    WE* bb = buf + B * PBUF;
+    static_assert(B == 0, "only bin 0 is staged");
+    WE* bb = buf;
     if (pred) bb[c[B] + __popc(m & lanemask_lt())] = v;
     c[B] += __popc(m);
     if (c[B] >= 32) {
@@ -474,6 +485,19 @@ __device__ __forceinline__ int32_t row_split(const Params& p, int32_t v, int64_t
     else hi = mid;
   }
   return (int32_t)(lo - beg);
+}
+
+// Same, one dependent level for short rows: the first 8 entries are loaded together.
+__device__ __forceinline__ int32_t split_fast(const Params& p, int32_t v, int64_t beg, int64_t end) {
+  const int64_t deg = end - beg;
+  int32_t w[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) w[u] = u < deg ? ldc(p.ci, beg + u) : 0x7fffffff;
+  int32_t k = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) k += w[u] < v;
+  if (k < 8 || deg <= 8) return k;
+  return 8 + row_split(p, v, beg + 8, end);
 }
 
 template <class S, int POL, bool CW>

@@ -13,8 +13,10 @@ namespace gcdev {
 // so First-Fit gives 1 to every vertex), plane-0 mask byte = 0.  With 8- or 16-bit state
 // words a vertex of degree > NARROW_MAX_DEG makes the run restart with 32-bit words
 // (ST_NEED32); 8-bit words restart with 16-bit ones when a colour > 127 appears (Phase A).
-template <class S, bool PUSH>
-__device__ __forceinline__ void prologue_count(const Params& p) {
+// Dense start (p.dense_div): also the split of every vertex (ksplit, one dependent level for
+// rows <= 8, else binary search) and the static list of the heavy vertices (bin 1).
+template <class S, int POL, bool PUSH>
+__device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
   __shared__ uint32_t s_cnt[NBIN];
   if (threadIdx.x < NBIN) s_cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -26,17 +28,36 @@ __device__ __forceinline__ void prologue_count(const Params& p) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
     int b = -1;
+    WE e;
     if (act) {
-      const int64_t deg = ldr(p.rp, v + 1) - ldr(p.rp, v);
+      e.v = (int32_t)(p.v_base + v);
+      e.beg = ldr(p.rp, v);
+      const int64_t end = ldr(p.rp, v + 1);
+      const int64_t deg = end - e.beg;
       if (sizeof(S) < 4 && deg > NARROW_MAX_DEG) wide = true;
       b = bin_of(p, deg);
       sts(st + p.v_base + v, 1u);
       if (PUSH) sts(p.fmp + v, 0u);
+      e.k = 0;
+      if (dense && POL != DEGREE) {
+        e.k = b == 0 ? split_fast(p, e.v, e.beg, end) : row_split(p, e.v, e.beg, end);
+        p.ksplit[v] = e.k;
+      }
     }
 #pragma unroll
     for (int k = 0; k < NBIN; ++k) {
       const unsigned m = __ballot_sync(FULL, b == k);
       if (m && lane == 0) atomicAdd(&s_cnt[k], (uint32_t)__popc(m));
+    }
+    if (dense) {
+      const unsigned m = __ballot_sync(FULL, b == 1);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t pos = 0;
+        if (lane == leader) pos = atomicAdd(&p.info->cursor[1], (uint32_t)__popc(m));
+        pos = __shfl_sync(FULL, pos, leader);
+        if (b == 1) stw(p.heavy + pos + __popc(m & lanemask_lt()), e);
+      }
     }
   }
   if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED32);
@@ -186,6 +207,15 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
   }
 }
 
+// reset the counters round r+1 will push into and the work queues it will pop from
+// (last used in round r-2)
+__device__ __forceinline__ void reset_next(const Params& p, uint32_t r) {
+  if (blockIdx.x == 0 && threadIdx.x < NBIN) {
+    p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
+    p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
+  }
+}
+
 template <class S, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const WE* W, Work& wk) {
   __shared__ uint32_t s_win[2];
@@ -193,18 +223,101 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
   uint32_t nb[NBIN];
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
-  // reset the counters round r+1 will push into and the work queues it will pop from
-  // (last used in round r-2)
-  if (blockIdx.x == 0 && threadIdx.x < NBIN) {
-    p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
-    p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
-  }
+  reset_next(p, r);
   if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
   if (PUSH) {
     zero_plane(p, r);
     phase_a_mask<S, CW>(p, bins, W, nb, wk);
   } else {
     phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
+  }
+}
+
+// Dense rounds (large |W|): W_r is implicit — every vertex whose state word is not committed —
+// and Phase A walks all n state words in id order: 16 consecutive vertices per thread, their
+// state words and plane-0 mask bytes read and the state words written back as 16-byte vectors
+// (no other thread touches these words during Phase A; committed words are written back
+// unchanged).  A vertex whose plane 0 is full reads its other planes one by one.
+__device__ __forceinline__ uint4 ldv(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stv(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <class S, bool CW>
+__device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work& wk) {
+  S* st = (S*)p.st;
+  reset_next(p, r);
+  if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
+    const uint32_t cur = r % 3;
+    wk.v[W_A_VERT] += (unsigned long long)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+  }
+  zero_plane(p, r);
+  const int lane = threadIdx.x & 31;
+  const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
+  const int64_t ngroups = ((int64_t)p.n + 15) / 16;
+  const int64_t g0 = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31);
+  for (int64_t gb = g0; gb < ngroups; gb += nthreads) {
+    const int64_t g = gb + lane;
+    const int64_t v0 = g * 16;
+    uint32_t fb = 0;
+    if (g < ngroups) {
+      constexpr int NW = 4 * (int)sizeof(S);          // 32-bit words holding 16 state words
+      constexpr int PER = 4 / (int)sizeof(S);          // state words per 32-bit word
+      constexpr uint32_t SMASK = sizeof(S) == 4 ? 0xffffffffu : ((1u << (8 * sizeof(S))) - 1u);
+      uint32_t w[NW];
+#pragma unroll
+      for (int i = 0; i < (int)sizeof(S); ++i) {
+        const uint4 q = ldv(st + v0 + i * (16 / sizeof(S)));
+        w[4 * i] = q.x;
+        w[4 * i + 1] = q.y;
+        w[4 * i + 2] = q.z;
+        w[4 * i + 3] = q.w;
+      }
+      const uint4 pl = ldv(p.fmp + v0);
+      const uint32_t pw[4] = {pl.x, pl.y, pl.z, pl.w};
+      bool dirty = false;
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        const int wi = h / PER, sh = (h % PER) * 8 * (int)sizeof(S);
+        const uint32_t sv = (w[wi] >> sh) & SMASK;
+        if (v0 + h < p.n && !(sv & SW<S>::COMMIT)) {
+          const uint32_t b0 = (pw[h >> 2] >> ((h & 3) * 8)) & 0xffu;
+          const uint32_t t = b0 != 0xffu ? (uint32_t)__ffs(b0 ^ 0xffu) : plane_firstfit(p, (int32_t)(v0 + h));
+          if (t == 0) {
+            fb |= 1u << h;
+          } else {
+            if (sizeof(S) == 1 && t > SW<S>::CMASK) atomicExch(&p.info->status, (uint32_t)ST_NEED16);
+            w[wi] = (w[wi] & ~(SMASK << sh)) | ((t & SMASK) << sh);
+            dirty = true;
+          }
+        }
+      }
+      if (dirty) {
+#pragma unroll
+        for (int i = 0; i < (int)sizeof(S); ++i)
+          stv(st + v0 + i * (16 / sizeof(S)), make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+      }
+    }
+    // colours beyond the planes: the whole warp, one vertex at a time (exact, reading C7)
+    unsigned m = __ballot_sync(FULL, fb != 0);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      uint32_t f = __shfl_sync(FULL, fb, src);
+      const int64_t sv0 = __shfl_sync(FULL, v0, src);
+      while (f) {
+        const int h = __ffs(f) - 1;
+        f &= f - 1;
+        const int32_t u = (int32_t)(sv0 + h);
+        uint32_t t = 8u * p.np + 1u;
+        if (sizeof(S) > 1 || t <= SW<S>::CMASK) t = firstfit_warp<S, CW>(p, u, t, wk, lane);
+        if (lane == 0) store_tent<S>(p, st, u, t);
+      }
+    }
   }
 }
 
@@ -252,18 +365,140 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
   return o;
 }
 
-// bin 0 (degree <= t3).  Every lane takes one vertex of the warp's chunk; the conflict scans
-// of all 32 vertices then advance together in passes over the flattened segments: pass 1
-// examines the first 4 positions of every scan range (the nearest lower ids, where most
-// conflicts are), later passes 12, 48, 192, ... more, so that early exit is kept for the
-// losers while all lanes stay busy.  A vertex with a hit loses (pushed to W_out); a vertex
-// whose range is exhausted wins: it commits and its row is scattered into the forbidden
-// masks of its neighbours, again as one flattened loop over all winners of the batch.
+// One batch of up to 32 vertices, one per lane (act).  The conflict scans of all of them
+// advance together in passes over the flattened segments: pass 1 examines the first 4
+// positions of every scan range (the nearest lower ids, where most conflicts are), later
+// passes 12, 48, 192, ... more, so that early exit is kept for the losers while all lanes stay
+// busy.  A vertex with a hit loses; a vertex whose range is exhausted wins: it commits and its
+// row is scattered into the forbidden masks of its neighbours, again as one flattened loop
+// over all winners of the batch.  e.k must be known (>= 0) unless POL == DEGREE; end = -1
+// when not yet read.  Returns the lane's state: 0 inactive, 1 lose, 2 win.
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, const WE& e, uint32_t tent, int64_t end,
+                                       Work& wk, int* s_first) {
+  S* st = (S*)p.st;
+  constexpr uint32_t CM = SW<S>::CMASK;
+  int64_t sbase = 0, dv = 0;
+  int sdir = 1;
+  uint32_t len = 0, pos = 0;
+  int state = 0;  // 0 inactive, 1 lose, 2 win, 3 undecided
+  if (act) {
+    if (POL != HIGHER_ID && end < 0) end = RP(p, e.v + 1);
+    const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+    sbase = sr.down ? sr.hi - 1 : sr.lo;
+    sdir = sr.down ? -1 : 1;
+    len = (uint32_t)(sr.hi - sr.lo);
+    if (POL == DEGREE) dv = end - e.beg;
+    state = len ? 3 : 2;
+  }
+  // conflict-scan passes
+  uint32_t cap = 4;
+  for (;;) {
+    const bool und = state == 3;
+    if (!__any_sync(FULL, und)) break;
+    const uint32_t Wn = und ? min(len - pos, cap) : 0u;
+    const uint32_t E = warp_incl_scan(Wn, lane);
+    const uint32_t T = __shfl_sync(FULL, E, 31);
+    if (CW) s_first[lane] = 0x7fffffff;
+    __syncwarp();
+    uint32_t lost = 0;
+    for (uint32_t f0 = 0; f0 < T; f0 += 32 * FLAT_U) {
+      int32_t w[FLAT_U];
+      int own[FLAT_U];
+      int64_t jj[FLAT_U];
+#pragma unroll
+      for (int u = 0; u < FLAT_U; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        const int o = flat_owner(E, f);
+        const int oc = o < 32 ? o : 31;
+        const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+        const uint32_t po = __shfl_sync(FULL, pos, oc);
+        const int64_t bo = __shfl_sync(FULL, sbase, oc);
+        const int dro = __shfl_sync(FULL, sdir, oc);
+        own[u] = f < T ? oc : -1;
+        jj[u] = (int64_t)(f - (Eo - Wo) + po);
+        w[u] = f < T ? ldc(p.ci, bo + dro * jj[u]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < FLAT_U; ++u) {
+        const int oc = own[u] < 0 ? 0 : own[u];
+        const uint32_t to = __shfl_sync(FULL, tent, oc);
+        const int32_t vo = __shfl_sync(FULL, e.v, oc);
+        const int64_t dvo = POL == DEGREE ? __shfl_sync(FULL, dv, oc) : 0;
+        const bool hit = own[u] >= 0 && (lds(st + w[u]) & CM) == to && recolors<POL>(p, vo, w[u], dvo);
+        if (hit) {
+          lost |= 1u << oc;
+          if (CW) atomicMin(&s_first[oc], (int)jj[u]);
+        }
+      }
+    }
+    lost = __reduce_or_sync(FULL, lost);
+    __syncwarp();
+    if (und) {
+      if (lost >> lane & 1u) {
+        state = 1;
+        if (CW) { const uint32_t ex = (uint32_t)s_first[lane] + 1; wk.v[W_B_EDGE] += ex; wk.v[W_B_GATHER] += ex; }
+      } else {
+        pos += Wn;
+        if (pos == len) {
+          state = 2;
+          if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
+        }
+      }
+    }
+    cap = cap < 1024 ? cap * 4 - (cap == 4 ? 4 : 0) : cap;  // 4, 12, 48, 192, 768, ...
+  }
+  // winners commit; the forbidden masks of their neighbours get their colour bit
+  const bool win = state == 2;
+  if (win) sts(st + e.v, tent | SW<S>::COMMIT);
+  if (PUSH) {
+    const bool sc = win && tent <= 8u * p.np;
+    if (sc && end < 0) end = RP(p, e.v + 1);
+    const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
+    if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wn; }
+    const uint32_t E = warp_incl_scan(Wn, lane);
+    const uint32_t T = __shfl_sync(FULL, E, 31);
+    for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
+      int32_t w[4];
+      uint32_t wb[4];
+      uint8_t* pl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        const int o = flat_owner(E, f);
+        const int oc = o < 32 ? o : 31;
+        const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+        const int64_t bo = __shfl_sync(FULL, e.beg, oc);
+        const uint32_t to = __shfl_sync(FULL, tent, oc);
+        pl[u] = p.fmp + (int64_t)((to - 1) >> 3) * p.plane;
+        wb[u] = 1u << ((to - 1) & 7);
+        w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
+      }
+      if (p.sfilter) {
+        uint32_t sw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sw[u] = w[u] >= 0 ? lds(st + w[u]) : SW<S>::COMMIT;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (!(sw[u] & SW<S>::COMMIT)) {
+            red_plane<S>(pl[u], w[u], wb[u]);
+            if (CW) wk.v[W_SCATTER_RED] += 1;
+          }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (w[u] >= 0) red_plane<S>(pl[u], w[u], wb[u]);
+      }
+    }
+  }
+  return state;
+}
+
+// Sparse bin 0 (degree <= t3): warps pop chunks of the worklist; one vertex per lane.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
                                              Work& wk, int* s_first) {
   S* st = (S*)p.st;
-  constexpr uint32_t CM = SW<S>::CMASK;
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * WARPS;
   const uint32_t ch = max(1u, min(64u, cnt / (4u * nwarps)));
@@ -271,139 +506,83 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
     const uint32_t cend = min(c0 + ch, cnt);
     for (uint32_t bse = c0; bse < cend; bse += 32) {
       const uint32_t i = bse + lane;
+      const bool act = i < cend;
       WE e;
       e.v = 0;
       e.k = 0;
       e.beg = 0;
       uint32_t tent = 0;
-      int64_t end = -1, sbase = 0, dv = 0;
-      int sdir = 1;
-      uint32_t len = 0, pos = 0;
-      int state = 0;  // 0 inactive, 1 lose, 2 win, 3 undecided
-      if (i < cend) {
+      int64_t end = -1;
+      if (act) {
         e = ldw(Wb + i);
-        tent = lds(st + e.v) & CM;
-        if (e.k < 0 || POL != HIGHER_ID) end = RP(p, e.v + 1);
-        if (e.k < 0 && POL != DEGREE) e.k = row_split(p, e.v, e.beg, end);
-        const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-        sbase = sr.down ? sr.hi - 1 : sr.lo;
-        sdir = sr.down ? -1 : 1;
-        len = (uint32_t)(sr.hi - sr.lo);
-        if (POL == DEGREE) dv = end - e.beg;
-        state = len ? 3 : 2;
-      }
-      // conflict-scan passes
-      uint32_t cap = 4;
-      for (;;) {
-        const bool und = state == 3;
-        if (!__any_sync(FULL, und)) break;
-        const uint32_t Wn = und ? min(len - pos, cap) : 0u;
-        const uint32_t E = warp_incl_scan(Wn, lane);
-        const uint32_t T = __shfl_sync(FULL, E, 31);
-        if (CW) s_first[lane] = 0x7fffffff;
-        __syncwarp();
-        uint32_t lost = 0;
-        for (uint32_t f0 = 0; f0 < T; f0 += 32 * FLAT_U) {
-          int32_t w[FLAT_U];
-          int own[FLAT_U];
-          int64_t jj[FLAT_U];
-#pragma unroll
-          for (int u = 0; u < FLAT_U; ++u) {
-            const uint32_t f = f0 + u * 32 + lane;
-            const int o = flat_owner(E, f);
-            const int oc = o < 32 ? o : 31;
-            const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
-            const uint32_t po = __shfl_sync(FULL, pos, oc);
-            const int64_t bo = __shfl_sync(FULL, sbase, oc);
-            const int dro = __shfl_sync(FULL, sdir, oc);
-            own[u] = f < T ? oc : -1;
-            jj[u] = (int64_t)(f - (Eo - Wo) + po);
-            w[u] = f < T ? ldc(p.ci, bo + dro * jj[u]) : 0;
-          }
-#pragma unroll
-          for (int u = 0; u < FLAT_U; ++u) {
-            const int oc = own[u] < 0 ? 0 : own[u];
-            const uint32_t to = __shfl_sync(FULL, tent, oc);
-            const int32_t vo = __shfl_sync(FULL, e.v, oc);
-            const int64_t dvo = POL == DEGREE ? __shfl_sync(FULL, dv, oc) : 0;
-            const bool hit = own[u] >= 0 && (lds(st + w[u]) & CM) == to && recolors<POL>(p, vo, w[u], dvo);
-            if (hit) {
-              lost |= 1u << oc;
-              if (CW) atomicMin(&s_first[oc], (int)jj[u]);
-            }
-          }
-        }
-        lost = __reduce_or_sync(FULL, lost);
-        __syncwarp();
-        if (und) {
-          if (lost >> lane & 1u) {
-            state = 1;
-            if (CW) { const uint32_t ex = (uint32_t)s_first[lane] + 1; wk.v[W_B_EDGE] += ex; wk.v[W_B_GATHER] += ex; }
-          } else {
-            pos += Wn;
-            if (pos == len) {
-              state = 2;
-              if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
-            }
-          }
-        }
-        cap = cap < 1024 ? cap * 4 - (cap == 4 ? 4 : 0) : cap;  // 4, 12, 48, 192, 768, ...
-      }
-      // winners commit; the forbidden masks of their neighbours get their colour bit
-      const bool win = state == 2;
-      if (win) sts(st + e.v, tent | SW<S>::COMMIT);
-      if (PUSH) {
-        const bool sc = win && tent <= 8u * p.np;
-        if (sc && end < 0) end = RP(p, e.v + 1);
-        const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
-        if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wn; }
-        const uint32_t E = warp_incl_scan(Wn, lane);
-        const uint32_t T = __shfl_sync(FULL, E, 31);
-        for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
-          int32_t w[4];
-          uint32_t wb[4];
-          uint8_t* pl[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t f = f0 + u * 32 + lane;
-            const int o = flat_owner(E, f);
-            const int oc = o < 32 ? o : 31;
-            const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
-            const int64_t bo = __shfl_sync(FULL, e.beg, oc);
-            const uint32_t to = __shfl_sync(FULL, tent, oc);
-            pl[u] = p.fmp + (int64_t)((to - 1) >> 3) * p.plane;
-            wb[u] = 1u << ((to - 1) & 7);
-            w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
-          }
-          if (p.sfilter) {
-            uint32_t sw[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) sw[u] = w[u] >= 0 ? lds(st + w[u]) : SW<S>::COMMIT;
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (!(sw[u] & SW<S>::COMMIT)) {
-                red_plane<S>(pl[u], w[u], wb[u]);
-                if (CW) wk.v[W_SCATTER_RED] += 1;
-              }
-          } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (w[u] >= 0) red_plane<S>(pl[u], w[u], wb[u]);
-          }
+        tent = lds(st + e.v) & SW<S>::CMASK;
+        if (e.k < 0 && POL != DEGREE) {
+          end = RP(p, e.v + 1);
+          e.k = row_split(p, e.v, e.beg, end);
         }
       }
+      const int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first);
       pu.template push<0, CW>(state == 1, e, lane, wk.v[W_PUSH]);
     }
   }
 }
 
+// Phase-B shared memory (one object per CTA, whichever phase function uses it).
+#ifndef GC_VPL
+#define GC_VPL 2
+#endif
+constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
+constexpr int WB = 32 * VPL;    // vertices per warp batch
+struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
+  int64_t sbase[WB];            // row position of scan step 0
+  uint32_t E[WB];               // inclusive prefix over the slots of the items of this pass
+  uint32_t pos[WB];             // scan steps done
+  int32_t k[WB];                // split (row start = sbase - k + 1 / sbase - k / sbase by policy)
+  uint32_t deg[WB];
+  int first[WB];                // work counters: first hit
+  uint32_t tent[WB];
+  uint32_t lost[VPL];
+};
+struct BSmem {
+  WE pbuf[WARPS][PBUF];   // per-warp push staging (Pusher, bin 0)
+  WideSeg seg[WARPS];     // dense batches
+  int first;              // conflict_cta
+  int32_t k;              // cta_vertex split broadcast
+  int cwfirst[WARPS][32]; // work counters: first hit per lane's vertex
+};
+__device__ __forceinline__ BSmem& bsmem() {
+  __shared__ BSmem s;
+  return s;
+}
+
+// One vertex of degree > t3 by the whole CTA (bin 1).  Returns true when it loses.
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent, Work& wk, int* s_first,
+                                           int32_t* s_k) {
+  S* st = (S*)p.st;
+  const int64_t end = RP(p, e.v + 1);
+  if (e.k < 0 && POL != DEGREE) {
+    if (threadIdx.x == 0) *s_k = row_split(p, e.v, e.beg, end);
+    __syncthreads();
+    e.k = *s_k;
+    __syncthreads();
+  }
+  const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
+  const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, s_first);
+  if (!lose) {
+    if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
+    if (PUSH && tent <= 8u * p.np) {
+      scatter<S, BLOCK, CW>(p, tent, e.beg + threadIdx.x, end, wk);
+      if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+    }
+  }
+  return lose;
+}
+
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const WE* W, WE* Wout,
                                         Work& wk) {
-  __shared__ WE s_pbuf[WARPS][NBIN * PBUF];
-  __shared__ int s_first;
-  __shared__ int32_t s_k;
-  __shared__ int s_cwfirst[CW ? WARPS : 1][32];
+  BSmem& sm = bsmem();
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   uint32_t nb[NBIN];
@@ -416,7 +595,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   }
   uint32_t* cnt_next = &p.info->cnt[nxt][0];
   Pusher pu;
-  pu.init(s_pbuf[warp], Wout, cnt_next, bins);
+  pu.init(sm.pbuf[warp], Wout, cnt_next, bins);
 
   // bin 1 first (one CTA per vertex, high degrees: the longest items start early), then the
   // dynamic bin-0 queue fills the gaps
@@ -426,32 +605,309 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
     for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       WE e = ldw(Wb + i);
       const uint32_t tent = lds(st + e.v) & SW<S>::CMASK;
-      const int64_t end = RP(p, e.v + 1);
-      if (e.k < 0 && POL != DEGREE) {
-        if (threadIdx.x == 0) s_k = row_split(p, e.v, e.beg, end);
-        __syncthreads();
-        e.k = s_k;
-        __syncthreads();
+      if (cta_vertex<S, POL, PUSH, CW>(p, e, tent, wk, &sm.first, &sm.k) && threadIdx.x == 0) {
+        stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
+        if (CW) wk.v[W_PUSH] += 1;
       }
-      const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-      const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, &s_first);
-      if (lose) {
-        if (threadIdx.x == 0) {
+      __syncthreads();
+    }
+  }
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk, sm.cwfirst[warp]);
+  pu.template flush<CW>(lane, wk.v[W_PUSH]);
+}
+
+// Dense batch: WB consecutive vertices per warp, VPL per lane (slots lane*VPL .. +VPL-1), so
+// that every dependent level of the batch (state words / row offsets / splits, then col_idx,
+// then the neighbours' state words, then the scatter) has VPL x more independent loads in flight
+// than one vertex per lane.  The per-slot data live in a shared-memory table; the flattened item
+// loop finds an item's slot by binary search over the prefix sums.  Same passes as batch_b.
+__device__ __forceinline__ int seg_owner(const uint32_t* E, uint32_t f) {
+  int o = 0;
+#pragma unroll
+  for (int b = WB / 2; b; b >>= 1)
+    if (E[o + b - 1] <= f) o += b;
+  return o;
+}
+// Writes the slots' E/W for the given per-lane W values; returns the total.
+__device__ __forceinline__ uint32_t seg_prefix(WideSeg& sg, const uint32_t (&Wh)[VPL], int lane) {
+  uint32_t tot = 0;
+#pragma unroll
+  for (int h = 0; h < VPL; ++h) tot += Wh[h];
+  const uint32_t incl = warp_incl_scan(tot, lane);
+  uint32_t run = incl - tot;
+#pragma unroll
+  for (int h = 0; h < VPL; ++h) {
+    run += Wh[h];
+    sg.E[lane * VPL + h] = run;
+  }
+  __syncwarp();
+  return __shfl_sync(FULL, incl, 31);
+}
+
+template <int POL>
+__device__ __forceinline__ int64_t seg_beg(const WideSeg& sg, int o) {
+  return POL == HIGHER_ID ? sg.sbase[o] - sg.k[o] + 1 : (POL == LOWER_ID ? sg.sbase[o] - sg.k[o] : sg.sbase[o]);
+}
+template <int POL>
+__device__ __forceinline__ uint32_t seg_len(const WideSeg& sg, int o) {
+  return POL == HIGHER_ID ? (uint32_t)sg.k[o] : (POL == LOWER_ID ? sg.deg[o] - (uint32_t)sg.k[o] : sg.deg[o]);
+}
+
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t base, uint32_t cend, WideSeg& sg,
+                                             bool push_out, Pusher& pu, uint32_t& lost_cnt, Work& wk) {
+  S* st = (S*)p.st;
+  constexpr uint32_t CM = SW<S>::CMASK;
+  constexpr int DIR = POL == HIGHER_ID ? -1 : 1;
+  const uint32_t v0 = base + lane * VPL;
+  // level 1: state words, row offsets, splits of the lane's VPL vertices (independent loads)
+  uint32_t states = 0;  // 8 bits per slot: 0 inactive, 1 lose, 2 win, 3 undecided
+  {
+    uint32_t sw[VPL];
+    int64_t rpv[VPL + 1];
+    int32_t kv[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) sw[h] = v0 + h < cend ? lds(st + v0 + h) : SW<S>::COMMIT;
+#pragma unroll
+    for (int h = 0; h <= VPL; ++h) rpv[h] = v0 + h <= cend ? ldr(p.rp, (int64_t)v0 + h) : 0;
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) kv[h] = (POL != DEGREE && v0 + h < cend) ? ldks(p.ksplit + v0 + h) : 0;
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      const int64_t beg = rpv[h], deg = rpv[h + 1] - rpv[h];
+      const bool act = v0 + h < cend && !(sw[h] & SW<S>::COMMIT) && deg <= (int64_t)p.t3;
+      sg.sbase[sl] = POL == HIGHER_ID ? beg + kv[h] - 1 : (POL == LOWER_ID ? beg + kv[h] : beg);
+      sg.k[sl] = kv[h];
+      sg.deg[sl] = (uint32_t)deg;
+      sg.tent[sl] = sw[h] & CM;
+      sg.pos[sl] = 0;
+      if (act) {
+        const uint32_t len = POL == HIGHER_ID ? (uint32_t)kv[h] : (POL == LOWER_ID ? (uint32_t)(deg - kv[h]) : (uint32_t)deg);
+        states |= (len ? 3u : 2u) << (8 * h);
+      }
+    }
+  }
+  __syncwarp();
+  // pass 1, lane-local: the first PROBE positions of the lane's own VPL scan ranges (no owner
+  // search; VPL x PROBE independent loads per lane).  Later passes are flattened.
+  {
+    int32_t w[VPL][PROBE];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      const bool und = ((states >> (8 * h)) & 0xffu) == 3u;
+      const uint32_t len = und ? seg_len<POL>(sg, sl) : 0u;
+      const int64_t sb = sg.sbase[sl];
+#pragma unroll
+      for (int u = 0; u < PROBE; ++u) w[h][u] = (uint32_t)u < len ? ldc(p.ci, sb + (int64_t)DIR * u) : -1;
+    }
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      if (((states >> (8 * h)) & 0xffu) != 3u) continue;
+      const uint32_t t = sg.tent[sl];
+      int first = -1;
+#pragma unroll
+      for (int u = PROBE - 1; u >= 0; --u)
+        if (w[h][u] >= 0 && (lds(st + w[h][u]) & CM) == t &&
+            recolors<POL>(p, (int32_t)(base + sl), w[h][u], (int64_t)sg.deg[sl]))
+          first = u;
+      const uint32_t len = seg_len<POL>(sg, sl);
+      if (first >= 0) {
+        states ^= 2u << (8 * h);  // 3 -> 1
+        if (CW) { wk.v[W_B_EDGE] += first + 1; wk.v[W_B_GATHER] += first + 1; }
+      } else {
+        const uint32_t np = len < (uint32_t)PROBE ? len : (uint32_t)PROBE;
+        sg.pos[sl] = np;
+        if (np == len) {
+          states ^= 1u << (8 * h);  // 3 -> 2
+          if (CW) { wk.v[W_B_EDGE] += np; wk.v[W_B_GATHER] += np; }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // conflict-scan passes (levels 2-3: col_idx of the scan positions, then their state words)
+  uint32_t cap = 12;
+  for (;;) {
+    const bool any = ((states | states >> 1) & 0x01010101u & (states & (states >> 1))) != 0;  // some slot == 3
+    if (!__any_sync(FULL, any)) break;
+    if (lane < VPL) sg.lost[lane] = 0;
+    uint32_t Wh[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      Wh[h] = ((states >> (8 * h)) & 0xffu) == 3u ? min(seg_len<POL>(sg, sl) - sg.pos[sl], cap) : 0u;
+      if (CW) sg.first[sl] = 0x7fffffff;
+    }
+    const uint32_t T = seg_prefix(sg, Wh, lane);
+    for (uint32_t f0 = 0; f0 < T; f0 += 32 * FLAT_U) {
+      int32_t w[FLAT_U];
+      int own[FLAT_U];
+      uint32_t jj[FLAT_U];
+#pragma unroll
+      for (int u = 0; u < FLAT_U; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        own[u] = -1;
+        w[u] = 0;
+        jj[u] = 0;
+        if (f < T) {
+          const int o = seg_owner(sg.E, f);
+          own[u] = o;
+          jj[u] = f - (o ? sg.E[o - 1] : 0u) + sg.pos[o];
+          w[u] = ldc(p.ci, sg.sbase[o] + (int64_t)DIR * jj[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < FLAT_U; ++u) {
+        if (own[u] >= 0) {
+          const int o = own[u];
+          const bool hit = (lds(st + w[u]) & CM) == sg.tent[o] &&
+                           recolors<POL>(p, (int32_t)(base + o), w[u], (int64_t)sg.deg[o]);
+          if (hit) {
+            atomicOr(&sg.lost[o >> 5], 1u << (o & 31));
+            if (CW) atomicMin(&sg.first[o], (int)jj[u]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      if (((states >> (8 * h)) & 0xffu) != 3u) continue;
+      if (sg.lost[sl >> 5] >> (sl & 31) & 1u) {
+        states ^= 2u << (8 * h);  // 3 -> 1
+        if (CW) { const uint32_t ex = (uint32_t)sg.first[sl] + 1; wk.v[W_B_EDGE] += ex; wk.v[W_B_GATHER] += ex; }
+      } else {
+        const uint32_t np = sg.pos[sl] + Wh[h];
+        sg.pos[sl] = np;
+        if (np == seg_len<POL>(sg, sl)) {
+          states ^= 1u << (8 * h);  // 3 -> 2
+          if (CW) { wk.v[W_B_EDGE] += np; wk.v[W_B_GATHER] += np; }
+        }
+      }
+    }
+    __syncwarp();
+    cap = cap < 1024 ? cap * 4 : cap;  // 12, 48, 192, 768, ...
+  }
+  // commit: winners set the top bit of their own state word
+#pragma unroll
+  for (int h = 0; h < VPL; ++h)
+    if (((states >> (8 * h)) & 0xffu) == 2u) sts(st + v0 + h, sg.tent[lane * VPL + h] | SW<S>::COMMIT);
+  // level 4: scatter of the winners' rows into the forbidden masks (flattened)
+  if (PUSH) {
+    uint32_t Wh[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      Wh[h] = ((states >> (8 * h)) & 0xffu) == 2u && sg.tent[sl] <= 8u * p.np ? sg.deg[sl] : 0u;
+      if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wh[h]; }
+    }
+    const uint32_t T = seg_prefix(sg, Wh, lane);
+    for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
+      int32_t w[4];
+      int own[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        own[u] = 0;
+        w[u] = -1;
+        if (f < T) {
+          const int o = seg_owner(sg.E, f);
+          own[u] = o;
+          w[u] = ldc(p.ci, seg_beg<POL>(sg, o) + (f - (o ? sg.E[o - 1] : 0u)));
+        }
+      }
+      uint32_t skip = 0;
+      if (p.sfilter) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (w[u] >= 0 && (lds(st + w[u]) & SW<S>::COMMIT)) skip |= 1u << u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (w[u] < 0 || (skip >> u & 1u)) continue;
+        const uint32_t t = sg.tent[own[u]];
+        red_plane<S>(p.fmp + (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
+        if (CW && p.sfilter) wk.v[W_SCATTER_RED] += 1;
+      }
+    }
+    __syncwarp();
+  }
+  // losers: counted, or pushed into W_out (split known) when round r+1 runs sparse
+  if (push_out) {
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      const int sl = lane * VPL + h;
+      WE e;
+      e.v = (int32_t)(v0 + h);
+      e.k = sg.k[sl];
+      e.beg = seg_beg<POL>(sg, sl);
+      pu.template push<0, CW>(((states >> (8 * h)) & 0xffu) == 1u, e, lane, wk.v[W_PUSH]);
+    }
+  } else {
+    uint32_t c = 0;
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) c += ((states >> (8 * h)) & 0xffu) == 1u;
+    lost_cnt += __reduce_add_sync(FULL, c);
+  }
+  __syncwarp();
+}
+
+// Dense Phase B: W_r = all uncommitted vertices.  The heavy vertices (degree > t3, a static
+// list built by the ingest) are taken one CTA each; the others by warps popping chunks of
+// consecutive ids (coalesced state words, row offsets and splits; consecutive rows are
+// contiguous in col_idx).  Losers are only counted — or, when push_out (|W_r| small enough
+// that round r+1 runs sparse), pushed into W_out with the split already known.
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const Bins& bins, WE* Wout, bool push_out,
+                                              Work& wk) {
+  BSmem& sm = bsmem();
+  S* st = (S*)p.st;
+  const uint32_t cur = r % 3, nxt = (r + 1) % 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t tot = ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
+    if (CW) wk.v[W_B_VERT] += tot;
+  }
+  uint32_t* cnt_next = &p.info->cnt[nxt][0];
+  Pusher pu;
+  pu.init(sm.pbuf[warp], Wout, cnt_next, bins);
+  {
+    const uint32_t nh = bins.size[1];
+    WE* Ob = Wout + bins.off[1];
+    for (uint32_t i = blockIdx.x; i < nh; i += gridDim.x) {
+      WE e = ldw(p.heavy + i);
+      if (threadIdx.x == 0) sm.k = (int32_t)lds(st + e.v);  // one read, broadcast
+      __syncthreads();
+      const uint32_t s = (uint32_t)sm.k;
+      __syncthreads();
+      if (s & SW<S>::COMMIT) continue;  // uniform over the CTA
+      if (cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k) && threadIdx.x == 0) {
+        if (push_out) {
           stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
           if (CW) wk.v[W_PUSH] += 1;
-        }
-      } else {
-        if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
-        if (PUSH && tent <= 8u * p.np) {
-          scatter<S, BLOCK, CW>(p, tent, e.beg + threadIdx.x, end, wk);
-          if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
+        } else {
+          atomicAdd(&cnt_next[1], 1u);
         }
       }
       __syncthreads();
     }
   }
-  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk, s_cwfirst[CW ? warp : 0]);
-  pu.template flush<CW>(lane, wk.v[W_PUSH]);
+  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t ch = max((uint32_t)WB, min(2048u, ((uint32_t)p.n / (8u * nwarps)) / WB * WB));
+  uint32_t* q = &p.info->qctr[cur][0][0];
+  uint32_t lost_cnt = 0;
+  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < (uint32_t)p.n; c0 = pop_chunk(q, ch, lane)) {
+    const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
+    for (uint32_t bse = c0; bse < cend; bse += WB)
+      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, pu, lost_cnt, wk);
+  }
+  if (push_out) pu.template flush<CW>(lane, wk.v[W_PUSH]);
+  else if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
 }
 
 // |W_{r+1}| summed over bins (read after the barrier that ends Phase B of round r).
@@ -500,11 +956,13 @@ template <class S, int POL, bool PUSH, bool CW>
 __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
   Work wk;
   wk.zero();
-  prologue_count<S, PUSH>(p);
+  const bool dense0 = PUSH && p.dense_div != 0;
+  prologue_count<S, POL, PUSH>(p, dense0);
   if (!grid_sync(p)) return;
   Bins bins;
   bins.load(p);
-  prologue_scatter(p, bins);
+  if (!dense0) prologue_scatter(p, bins);
+  else if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = bins.size[threadIdx.x];
   if (!grid_sync(p)) return;
   const bool stamp = p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0;
   if (stamp) p.phase_ns[0] = globaltimer();
@@ -512,16 +970,28 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
   // The worklist pointers are re-read from DevInfo every round instead of being swapped in
   // registers: with loop-carried pointer swaps, ptxas (12.9) was observed to reuse the
   // uniform register holding one of them inside the grid barrier (truncated addresses).
+  // Rounds run dense (W_r implicit, id-order sweeps) while |W_r| * dense_div > n, then
+  // sparse (worklists); the round whose |W_r| first falls below pushes its losers.
   uint32_t r = 1;
+  bool dense = dense0;
   for (;;) {
     WE* Win = (WE*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
     WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
     if (r > 1) {
-      phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
+      if (dense) phase_a_dense<S, CW>(p, r, wk);
+      else phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
       if (!grid_sync(p)) return;
     }
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r - 1] = globaltimer();
-    phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
+    if (dense) {
+      const uint32_t cur = r % 3;
+      const uint64_t tot = (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+      const bool push_out = tot * p.dense_div <= (uint64_t)p.n;
+      phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, wk);
+      if (push_out) dense = false;
+    } else {
+      phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
+    }
     if (!grid_sync(p)) return;
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
     const uint32_t left = next_total(p, r);
@@ -542,7 +1012,7 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
 // GC_FLAG_HOST_ROUNDS: the same phases (32-bit state words), one non-cooperative launch
 // each, the host reading |W_{r+1}| after every round ("CPU ... controlling the progress").
 template <bool PUSH>
-__global__ void __launch_bounds__(BLOCK) k_prologue_count(Params p) { prologue_count<uint32_t, PUSH>(p); }
+__global__ void __launch_bounds__(BLOCK) k_prologue_count(Params p) { prologue_count<uint32_t, HIGHER_ID, PUSH>(p, false); }
 __global__ void __launch_bounds__(BLOCK) k_prologue_scatter(Params p) {
   Bins b;
   b.load(p);

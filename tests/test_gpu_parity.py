@@ -86,15 +86,20 @@ def test_parity_variants(gc, kw):
 
 
 @pytest.mark.parametrize("env", [dict(GC_STATE_BYTES="2"), dict(GC_STATE_BYTES="4"),
-                                 dict(GC_SCATTER_FILTER="1"), dict(GC_L2_PERSIST="0")],
+                                 dict(GC_SCATTER_FILTER="1"), dict(GC_L2_PERSIST="0"),
+                                 dict(GC_DENSE_DIV="0"), dict(GC_DENSE_DIV="1"),
+                                 dict(GC_DENSE_DIV="1000000000")],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_parity_env_variants(gc, env, monkeypatch):
     """Forced state-word widths, filtered commit scatter, no L2 window: same result."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    for g in (wl.rmat(13, 8, seed=7), wl.rmat(11, 16, wl.GRAPH500, 5), wl.complete(70), wl.complete(130)):
+    for g in (wl.rmat(13, 8, seed=7), wl.rmat(11, 16, wl.GRAPH500, 5), wl.complete(70), wl.complete(130),
+              wl.disjoint_union(wl.star(3000), wl.mesh2d(40, 30, 0.3), wl.star(2000, center_last=True)),
+              wl.stencil27(9, 7, 5)):
         for pol in POLICIES:
             _check(gc, g, pol)
+            _check(gc, g, pol, warp_bin_max=8)
         _check(gc, g, "higher_id", host_rounds=True)
 
 
