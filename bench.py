@@ -110,27 +110,31 @@ class ClockSampler:
                 "samples": len(s)}
 
 
-def algorithmic_bytes(work, n, narrow=True):
-    """Bytes the implemented algorithm must move per launch (DESIGN.md §7 per-unit table).
+def algorithmic_bytes(work, n):
+    """Bytes the implemented algorithm must move per launch (DESIGN.md §7 per-unit table),
+    from the exact work counters of an instrumented run (a pure function of the graph).
 
-    Per-unit figures (sw = state word, 2 B for Delta < 32767 else 4 B; WE = 16-B worklist
-    entry {v, split, row start}):
-      ingest      per vertex   : 2x row_ptr pair (32) + sw + fm + fm2 (8) + WE write (16)
-      Phase A     per vertex   : v (4) + fm (4) + sw write
-                  per fallback neighbour : col (4) + sw
-      Phase B     per vertex   : WE (16) + own sw + row_ptr end (8)
-                  per examined position  : col (4) + sw gather
-                  per loser    : WE push (16);  per winner : sw commit
-      scatter     per edge     : col (4) + forbidden-mask RED (4)
-      finalize    per vertex   : sw read + colour write (4)
+    sw = state-word bytes (1 while colours <= 127); WE = 16-B worklist entry; plane = 1-B
+    forbidden-colour byte; RED = 4-B atomic on the word holding a plane byte.
+      ingest   per vertex : row_ptr 8 + split 4 + sw + plane 1 + one col_idx sector (32)
+      Phase A  dense, per vertex swept   : sw + plane 1
+               sparse, per entry         : WE 16 + plane 1
+               per pending vertex        : sw (tentative colour written)
+               per fallback neighbour    : col 4 + sw
+      Phase B  dense, per vertex swept   : sw;  per pending vertex : row_ptr 8 + split 4
+               sparse, per entry         : WE 16 + sw
+               per examined position     : col 4 + sw
+               per vertex (commit, once) : sw;  per pushed loser : WE 16
+               per scatter edge          : col 4 + RED 4
+      finalize per vertex : sw + colour 4
     """
-    sw = 2 if narrow else 4
-    losers = work["pushes"]
-    winners = work["phase_b_vertices"] - losers
-    return ((32 + sw + 8 + 16) * n
-            + (8 + sw) * work["phase_a_vertices"] + (4 + sw) * work["phase_a_edges"]
-            + (16 + sw + 8) * work["phase_b_vertices"] + (4 + sw) * work["phase_b_edges"]
-            + 16 * losers + sw * winners
+    sw = int(work.get("state_bytes") or 1)
+    dense_b_pending = work["phase_b_vertices"] - work["sparse_b_entries"]
+    return ((8 + 4 + sw + 1 + 32) * n
+            + (sw + 1) * work["dense_a_swept"] + 17 * work["sparse_a_entries"]
+            + sw * work["phase_a_vertices"] + (4 + sw) * work["phase_a_edges"]
+            + sw * work["dense_b_swept"] + 12 * dense_b_pending + (16 + sw) * work["sparse_b_entries"]
+            + (4 + sw) * work["phase_b_edges"] + sw * n + 16 * work["pushes"]
             + 8 * work["commit_scatter"]
             + (sw + 4) * n)
 
@@ -265,7 +269,7 @@ def run_ours(args):
     # untimed instrumented run: exact work counters -> algorithmic bytes per launch
     wres = gc.color(rp, ci, count_work=True, trace=True, **kw)
     work = wres.work
-    alg_bytes = algorithmic_bytes(work, n, narrow=g.max_degree() < 32767)
+    alg_bytes = algorithmic_bytes(work, n)
     verified = gc.verify(rp, ci, out) == -1
 
     for _ in range(args.warmup):
@@ -326,7 +330,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "u%d" % (8 * int(work.get("state_bytes") or 4)),
+            "data": "synthetic",
             "config": {"workload": args.config, "n": n, "m": m, "policy": args.policy,
                        "validate": False, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                        "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB); no flush" % ((8 * (n + 1) + 4 * m) / 1e9)},

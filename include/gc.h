@@ -80,7 +80,12 @@ typedef struct gc_work {
   uint64_t commit_scatter;     /* neighbour entries visited by the commit scatters */
   uint64_t pushes;             /* vertices pushed into W_out over the run */
   uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters */
-  uint64_t reserved[8];
+  uint64_t dense_a_swept;      /* vertices swept by dense (id-order) Phase A passes */
+  uint64_t dense_b_swept;      /* vertices swept by dense Phase B passes */
+  uint64_t sparse_a_entries;   /* worklist entries read by sparse Phase A passes */
+  uint64_t sparse_b_entries;   /* worklist entries read by sparse Phase B passes */
+  uint64_t state_bytes;        /* width of the state words of the final attempt (1, 2 or 4) */
+  uint64_t reserved[3];
 } gc_work;
 
 typedef struct gc_opts {

@@ -43,7 +43,9 @@ class Work(ctypes.Structure):
                 ("phase_b_vertices", ctypes.c_uint64), ("phase_b_edges", ctypes.c_uint64),
                 ("phase_b_gathers", ctypes.c_uint64), ("commit_scatter", ctypes.c_uint64),
                 ("pushes", ctypes.c_uint64), ("scatter_reds", ctypes.c_uint64),
-                ("reserved", ctypes.c_uint64 * 8)]
+                ("dense_a_swept", ctypes.c_uint64), ("dense_b_swept", ctypes.c_uint64),
+                ("sparse_a_entries", ctypes.c_uint64), ("sparse_b_entries", ctypes.c_uint64),
+                ("state_bytes", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 3)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}

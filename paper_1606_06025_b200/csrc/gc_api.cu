@@ -482,6 +482,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     return cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
   };
+  int sbytes = 4, sbytes_used = 4;
   if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
     // ---- persistent cooperative kernel: the whole run in one launch
     if (!prop.coop) {
@@ -491,7 +492,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     // 8-bit state words first; a colour > 127 makes the kernel stop at the next barrier with
     // ST_NEED16 and a vertex of degree > 32766 stops it in its prologue with ST_NEED32; the
     // run is then repeated with the wider words (at most two restarts).
-    int sbytes = 1;
+    sbytes = 1;
     if (const char* sw = getenv("GC_STATE_BYTES")) {  // diagnostics: force a width
       const int f = atoi(sw);
       if (f == 1 || f == 2 || f == 4) sbytes = f;
@@ -513,6 +514,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       uint32_t status = 0;
       CK(cudaMemcpyAsync(&status, &((DevInfo*)info)->status, sizeof(status), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      sbytes_used = sbytes;
       if (status == ST_NEED16 && sbytes < 2) sbytes = 2;
       else if (status == ST_NEED32 && sbytes < 4) sbytes = 4;
       else break;
@@ -617,6 +619,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     o.work->commit_scatter = hinfo.work[W_SCATTER];
     o.work->pushes = hinfo.work[W_PUSH];
     o.work->scatter_reds = hinfo.work[W_SCATTER_RED];
+    o.work->dense_a_swept = hinfo.work[W_DA_SWEEP];
+    o.work->dense_b_swept = hinfo.work[W_DB_SWEEP];
+    o.work->sparse_a_entries = hinfo.work[W_SA_ENT];
+    o.work->sparse_b_entries = hinfo.work[W_SB_ENT];
+    o.work->state_bytes = (uint64_t)sbytes_used;
   }
   *num_colors = hinfo.num_colors;
   *rounds = hinfo.rounds;

@@ -224,7 +224,10 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
   reset_next(p, r);
-  if (CW && threadIdx.x == 0 && blockIdx.x == 0) wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
+  if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
+    wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
+    wk.v[W_SA_ENT] += (unsigned long long)nb[0] + nb[1];
+  }
   if (PUSH) {
     zero_plane(p, r);
     phase_a_mask<S, CW>(p, bins, W, nb, wk);
@@ -254,6 +257,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work&
   if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
     const uint32_t cur = r % 3;
     wk.v[W_A_VERT] += (unsigned long long)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+    wk.v[W_DA_SWEEP] += (unsigned long long)p.n;
   }
   zero_plane(p, r);
   const int lane = threadIdx.x & 31;
@@ -591,7 +595,10 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1];
-    if (CW) wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1];
+    if (CW) {
+      wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1];
+      wk.v[W_SB_ENT] += (unsigned long long)nb[0] + nb[1];
+    }
   }
   uint32_t* cnt_next = &p.info->cnt[nxt][0];
   Pusher pu;
@@ -871,7 +878,10 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const uint32_t tot = ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
-    if (CW) wk.v[W_B_VERT] += tot;
+    if (CW) {
+      wk.v[W_B_VERT] += tot;
+      wk.v[W_DB_SWEEP] += (unsigned long long)p.n;
+    }
   }
   uint32_t* cnt_next = &p.info->cnt[nxt][0];
   Pusher pu;

@@ -1,7 +1,9 @@
 set -u
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_default.log 2>&1; tail -1 gpurun_out/bench_default.log
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.log 2>&1; tail -1 gpurun_out/bench_reference.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_rmat24.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgr_persistent -s 2 -c 1 -o gpurun_out/prof_rmat24 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_rmat24.log 2>&1; tail -1 gpurun_out/bench_rmat24.log | cut -c1-600
 for c in stencil128 mesh8192; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_$c.log 2>&1; tail -1 gpurun_out/bench_$c.log | cut -c1-300; done
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.log 2>&1; tail -1 gpurun_out/bench_reference.log | cut -c1-300
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_rmat24.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+for c in ${NCU_CONFIGS:-rmat24}; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgr_persistent -s 2 -c 1 -o gpurun_out/prof_$c -f python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full_$c.log 2>&1; echo ncu2 $c rc=$?
+done
