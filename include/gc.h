@@ -85,7 +85,12 @@ typedef struct gc_work {
   uint64_t sparse_a_entries;   /* worklist entries read by sparse Phase A passes */
   uint64_t sparse_b_entries;   /* worklist entries read by sparse Phase B passes */
   uint64_t state_bytes;        /* width of the state words of the final attempt (1, 2 or 4) */
-  uint64_t reserved[3];
+  uint64_t phase_b_evaluated;  /* pending vertices whose conflict scan ran (dirty-set rounds skip
+                                  the clean ones) */
+  uint64_t dense_b_evaluated;  /* of which in dense rounds */
+  uint64_t dirty_marks;        /* dirty marks written (changed vertices and their successors) */
+  uint64_t tent_changes;       /* tentative colours changed by Phase A */
+  uint64_t reserved[4];
 } gc_work;
 
 typedef struct gc_opts {

@@ -341,7 +341,13 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   // covers the hot per-vertex state: the state words (1, 2 or 4 bytes per vertex, placed
   // right before plane 0 whatever their width) and the first forbidden-colour planes.
   const int64_t pitch = (n + 255) / 256 * 256;
-  const uint32_t np = push ? (uint32_t)MAX_PLANES : 0u;
+  // up to MAX_PLANES planes (colours 1..512), at most ~16 GB of them; only the planes a run
+  // reaches are ever touched (plane k from round 8k on)
+  uint32_t np = push ? (uint32_t)MAX_PLANES : 0u;
+  if (push && (uint64_t)np * (uint64_t)pitch > (16ull << 30)) {
+    const uint64_t fit = (16ull << 30) / (uint64_t)pitch;
+    np = fit < 16 ? 16u : (uint32_t)fit;
+  }
   void* hot;
   CK(sc.alloc(&hot, (size_t)pitch * (4 + np)));
   planes = (uint8_t*)hot + 4 * pitch;
@@ -350,7 +356,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
   if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
   const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 512;
-  void *ksplit = nullptr, *heavy = nullptr;
+  void *ksplit = nullptr, *heavy = nullptr, *dirty = nullptr;
+  // dirty-set rounds: needs the per-vertex splits of the dense ingest
+  uint32_t n1 = 1;
+  if (const char* e = getenv("GC_N1")) n1 = (uint32_t)atoi(e);
+  if (!dense_div) n1 = 0;
   if (dense_div) {
     if (m < 0) {
       CK(cudaMemcpyAsync(&m, d_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -358,6 +368,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     }
     const int64_t hcap = m / ((int64_t)t3 + 1) + 1;  // vertices of degree > t3
     CK(sc.alloc(&ksplit, sizeof(int32_t) * (size_t)n));
+    if (n1) CK(sc.alloc(&dirty, (size_t)pitch));
     CK(sc.alloc(&heavy, sizeof(WE) * (size_t)(hcap < n ? hcap : n)));
   }
   CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
@@ -418,6 +429,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
   p.dense_div = dense_div;
   p.ksplit = (int32_t*)ksplit;
+  p.dirty = (uint8_t*)dirty;
+  p.n1 = dirty ? n1 : 0u;
+  p.davg2 = n > 0 && m > 0 ? (uint32_t)((m + 2 * n - 1) / (2 * n)) + 1u : 1u;  // successors + 1
+  p.n1gain = n > 0 ? (uint32_t)(m / (2 * n) < 8 ? m / (2 * n) : 8) : 0u;
   p.heavy = (WE*)heavy;
   p.timeout_ns = 60ull * 1000000000ull;
 
@@ -624,6 +639,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     o.work->sparse_a_entries = hinfo.work[W_SA_ENT];
     o.work->sparse_b_entries = hinfo.work[W_SB_ENT];
     o.work->state_bytes = (uint64_t)sbytes_used;
+    o.work->phase_b_evaluated = hinfo.work[W_B_EVAL];
+    o.work->dense_b_evaluated = hinfo.work[W_DB_EVAL];
+    o.work->dirty_marks = hinfo.work[W_MARK];
+    o.work->tent_changes = hinfo.work[W_TCHG];
   }
   *num_colors = hinfo.num_colors;
   *rounds = hinfo.rounds;

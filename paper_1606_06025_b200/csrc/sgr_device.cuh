@@ -52,10 +52,10 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int32_t NARROW_MAX_DEG = 32766;  // 16-bit state: colours <= Delta+1 <= 32767
 
 enum Policy { HIGHER_ID = 0, LOWER_ID = 1, DEGREE = 2 };
-constexpr int MAX_PLANES = 16;     // byte planes of forbidden colours: colours 1..128
+constexpr int MAX_PLANES = 64;     // byte planes of forbidden colours: colours 1..512
 enum Status { ST_OK = 0, ST_NEED16 = 2, ST_NO_CONVERGENCE = 3, ST_NEED32 = 4, ST_WATCHDOG = 5 };
 enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_SCATTER_RED,
-               W_DA_SWEEP, W_DB_SWEEP, W_SA_ENT, W_SB_ENT, W_N };
+               W_DA_SWEEP, W_DB_SWEEP, W_SA_ENT, W_SB_ENT, W_B_EVAL, W_DB_EVAL, W_MARK, W_TCHG, W_N };
 
 // State-word traits: top bit = committed, remaining bits = colour.
 template <class S> struct SW;
@@ -74,11 +74,12 @@ struct DevInfo {
   uint32_t status;
   uint32_t rounds;
   uint32_t num_colors;
-  uint32_t pad0;
+  uint32_t maxdeg;              // max degree (ingest)
   uint32_t binsize[NBIN];
   uint32_t cursor[NBIN];
   uint32_t cnt[3][NBIN];        // |W| per bin, triple-buffered by round (r % 3)
-  uint32_t pad1[8];
+  uint32_t chg[3];              // tentative colours changed by Phase A, by round (r % 3)
+  uint32_t pad1[5];
   uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
   unsigned long long wlp[2];    // the two worklist buffers (re-read every round, see sgr_persistent)
   unsigned long long work[W_N];
@@ -113,6 +114,10 @@ struct Params {
   uint32_t sfilter;             // commit scatter skips neighbours already committed
   uint32_t dense_div;           // dense rounds while |W_r| * dense_div > n (0: always sparse)
   int32_t* ksplit;              // dense mode: number of lower-id neighbours of every vertex
+  uint8_t* dirty;               // dirty-set rounds (N1): Phase B re-examines only marked vertices
+  uint32_t n1;                  // dirty-set rounds enabled
+  uint32_t davg2;               // average successors + 1 (m/2n + 1, rounded up): N1 cost model
+  uint32_t n1gain;              // min(m/2n, 8): N1 saving per clean vertex, in units of marks
   WE* heavy;                    // dense mode: the vertices of degree > t3 {v, split, row start}
   WE* wl0;                      // worklist buffers, n entries each, bin segments
   WE* wl1;
@@ -141,14 +146,27 @@ struct Work {
 // (createpolicy + ld/st/red .L2::cache_hint) were observed to make ptxas 12.9 (sm_100a)
 // emit code that clobbers live uniform registers in this kernel.
 // CSR: read-only for the whole kernel -> non-coherent path, not allocated in L1 (streamed).
+// GC_CS: the CSR streams are loaded evict-first in L2 as well (ld.global.cs.nc), so that they
+// do not push the per-vertex state words and forbidden-colour planes out of L2.
+#ifndef GC_CS
+#define GC_CS 1
+#endif
 __device__ __forceinline__ int32_t ldc(const int32_t* __restrict__ p, int64_t i) {
   int32_t v;
+#if GC_CS
+  asm("ld.global.cs.nc.b32 %0, [%1];" : "=r"(v) : "l"(p + i));
+#else
   asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p + i));
+#endif
   return v;
 }
 __device__ __forceinline__ int64_t ldr(const int64_t* __restrict__ p, int64_t i) {
   int64_t v;
+#if GC_CS
+  asm("ld.global.cs.nc.b64 %0, [%1];" : "=l"(v) : "l"(p + i));
+#else
   asm("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p + i));
+#endif
   return v;
 }
 // Everything written inside the run (worklists, state words, forbidden masks) is read with

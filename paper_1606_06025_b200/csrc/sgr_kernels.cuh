@@ -24,6 +24,7 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   bool wide = false;
+  uint32_t maxdeg = 0;
   for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
@@ -35,9 +36,11 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       const int64_t end = ldr(p.rp, v + 1);
       const int64_t deg = end - e.beg;
       if (sizeof(S) < 4 && deg > NARROW_MAX_DEG) wide = true;
+      maxdeg = max(maxdeg, (uint32_t)min(deg, (int64_t)0xffffffff));
       b = bin_of(p, deg);
       sts(st + p.v_base + v, 1u);
       if (PUSH) sts(p.fmp + v, 0u);
+      if (p.dirty) sts(p.dirty + v, 0u);
       e.k = 0;
       if (dense && POL != DEGREE) {
         e.k = b == 0 ? split_fast(p, e.v, e.beg, end) : row_split(p, e.v, e.beg, end);
@@ -61,6 +64,8 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
     }
   }
   if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED32);
+  maxdeg = __reduce_max_sync(FULL, maxdeg);
+  if (lane == 0 && maxdeg) atomicMax(&p.info->maxdeg, maxdeg);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.info->wlp[0] = (unsigned long long)p.wl0;
     p.info->wlp[1] = (unsigned long long)p.wl1;
@@ -99,6 +104,62 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
   if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = p.info->binsize[threadIdx.x];
 }
 
+// ---- warp-flattened segment loops
+// Each lane of a warp holds a segment of W_i items (a vertex's next stretch of its conflict
+// scan, or a winner's row for the commit scatter).  The warp walks the concatenation of all
+// segments 32 x FLAT_U items per step, so short and long segments share the lanes evenly
+// instead of one lane (or one vertex at a time) doing all of a segment's work.  Item f
+// belongs to the lane `owner` with E[owner-1] <= f < E[owner] (E = inclusive prefix sum of
+// W over the lanes, found by a 5-step binary search over shuffles).
+constexpr int FLAT_U = 2;     // items per lane per step (independent loads in flight)
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
+  int o = 0;
+#pragma unroll
+  for (int b = 16; b; b >>= 1)
+    if (__shfl_sync(FULL, E, o + b - 1) <= f) o += b;
+  return o;
+}
+
+// Phase shared memory (one object per CTA, whichever phase function uses it).
+#ifndef GC_VPL
+#define GC_VPL 2
+#endif
+constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
+constexpr int WB = 32 * VPL;    // vertices per warp batch
+struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
+  int64_t sbase[WB];            // row position of scan step 0
+  uint32_t E[WB];               // inclusive prefix over the slots of the items of this pass
+  uint32_t pos[WB];             // scan steps done
+  int32_t k[WB];                // split (row start = sbase - k + 1 / sbase - k / sbase by policy)
+  uint32_t deg[WB];
+  int first[WB];                // work counters: first hit
+  uint32_t tent[WB];
+  uint32_t lost[VPL];
+};
+struct BSmem {
+  WE pbuf[WARPS][PBUF];   // per-warp push staging (Pusher, bin 0)
+  union {
+    WideSeg seg[WARPS];     // dense Phase-B batches
+    int32_t clist[WARPS][512];  // dense Phase A: a warp's changed vertices (N1 marks)
+  };
+  int first;              // conflict_cta
+  int32_t k;              // cta_vertex split broadcast
+  int cwfirst[WARPS][32]; // work counters: first hit per lane's vertex
+};
+__device__ __forceinline__ BSmem& bsmem() {
+  __shared__ BSmem s;
+  return s;
+}
+
 // ---------------------------------------------------------------- a2: Phase A
 // Incremental-mask mode: every pending vertex is O(1) in the number of neighbours: its own
 // thread reads its plane bytes two planes at a time (independent loads) until a non-full one
@@ -124,37 +185,98 @@ __device__ __forceinline__ uint32_t plane_firstfit(const Params& p, int32_t v) {
   return 0;
 }
 
-template <class S, bool CW>
-__device__ __forceinline__ void phase_a_mask(const Params& p, const Bins& bins, const WE* W, const uint32_t* nb,
-                                             Work& wk) {
+// ---- dirty-set rounds (reading of the data-driven rationale P:453-462)
+// The Phase-B outcome of a pending vertex v depends only on tent(v) and on tent(w) of its
+// predecessors w (the neighbours that can make it recolour: lower ids for HIGHER_ID, higher
+// ids for LOWER_ID, all for DEGREE).  A vertex still pending lost last round; if neither its
+// tentative colour nor any predecessor's changed since, it loses again.  (A predecessor that
+// committed with colour c either was not v's conflict — no effect — or had c = tent(v), and
+// then c entered v's mask and tent(v) changed.)  So when Phase A changes tent(v) it marks v
+// and its successors dirty, and Phase B of a marking round examines only dirty vertices; the
+// others are losers as they stand.  Marks are set in Phase A and cleared by the Phase-B lane
+// that reads them; a round that does not mark examines every pending vertex.
+template <int POL, bool CW>
+__device__ __forceinline__ void mark_dirty(const Params& p, int32_t v, int64_t beg, int64_t end, int32_t k, Work& wk) {
+  const int64_t lo = POL == HIGHER_ID ? beg + k : beg;
+  const int64_t hi = POL == LOWER_ID ? beg + k : end;
+  sts(p.dirty + v, 1u);
+  for (int64_t e = lo; e < hi; e += 4) {
+    int32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = e + u < hi ? ldc(p.ci, e + u) : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (w[u] >= 0) sts(p.dirty + w[u], 1u);
+  }
+  if (CW) wk.v[W_MARK] += (unsigned long long)(hi - lo + 1);
+}
+
+// New tentative colour t of pending vertex v whose previous one is t_old: store it and, when
+// it changed and this round marks, mark v and its successors.
+template <class S, int POL, bool CW>
+__device__ __forceinline__ void tent_update(const Params& p, S* st, int32_t v, uint32_t t, uint32_t t_old, bool mark,
+                                            int64_t beg, int64_t end, int32_t k, uint32_t& nchg, Work& wk) {
+  if (t == t_old) return;
+  store_tent<S>(p, st, v, t);
+  ++nchg;
+  if (mark) {
+    if (beg < 0) {
+      beg = RP(p, v);
+      end = RP(p, v + 1);
+    }
+    if (end < 0) end = RP(p, v + 1);
+    if (k < 0 && POL != DEGREE) k = ldks(p.ksplit + v);
+    mark_dirty<POL, CW>(p, v, beg, end, k, wk);
+  }
+}
+
+__device__ __forceinline__ void flush_chg(const Params& p, uint32_t r, uint32_t nchg, Work& wk, bool cw) {
+  nchg = __reduce_add_sync(FULL, nchg);
+  if ((threadIdx.x & 31) == 0 && nchg) {
+    atomicAdd(&p.info->chg[r % 3], nchg);
+    if (cw) wk.v[W_TCHG] += nchg;
+  }
+}
+
+template <class S, int POL, bool CW>
+__device__ __forceinline__ void phase_a_mask(const Params& p, uint32_t r, const Bins& bins, const WE* W,
+                                             const uint32_t* nb, bool mark, Work& wk) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
+  uint32_t nchg = 0;
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) {
     const WE* Wb = W + bins.off[b];
     const uint32_t cnt = nb[b];
     for (uint32_t base = gw * 32; base < cnt; base += nw * 32) {
       const uint32_t i = base + lane;
-      int32_t v = 0;
+      WE e;
+      e.v = 0;
+      e.k = -1;
+      e.beg = -1;
+      uint32_t t_old = 0;
       bool fb = false;
       if (i < cnt) {
-        v = ldw_v(Wb + i);
-        const uint32_t t = plane_firstfit(p, v);
-        if (t) store_tent<S>(p, st, v, t);
+        e = ldw(Wb + i);
+        t_old = lds(st + e.v) & SW<S>::CMASK;
+        const uint32_t t = plane_firstfit(p, e.v);
+        if (t) tent_update<S, POL, CW>(p, st, e.v, t, t_old, mark, e.beg, -1, e.k, nchg, wk);
         else fb = true;
       }
       unsigned m = __ballot_sync(FULL, fb);
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
-        const int32_t u = __shfl_sync(FULL, v, src);
+        const int32_t u = __shfl_sync(FULL, e.v, src);
+        const uint32_t to = __shfl_sync(FULL, t_old, src);
         uint32_t t = 8u * p.np + 1u;  // > 127 when np = MAX_PLANES: 8-bit words restart
         if (sizeof(S) > 1 || t <= SW<S>::CMASK) t = firstfit_warp<S, CW>(p, u, t, wk, lane);
-        if (lane == 0) store_tent<S>(p, st, u, t);
+        if (lane == 0) tent_update<S, POL, CW>(p, st, u, t, to, mark, -1, -1, -1, nchg, wk);
       }
     }
   }
+  flush_chg(p, r, nchg, wk, CW);
 }
 
 // Plane k (colours 8k+1..8k+8) is zeroed in Phase A of round 8k, before any colour it holds
@@ -213,11 +335,13 @@ __device__ __forceinline__ void reset_next(const Params& p, uint32_t r) {
   if (blockIdx.x == 0 && threadIdx.x < NBIN) {
     p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
+    if (threadIdx.x == 0) p.info->chg[(r + 1) % 3] = 0;
   }
 }
 
-template <class S, bool PUSH, bool CW>
-__device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const WE* W, Work& wk) {
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins& bins, const WE* W, bool mark,
+                                        Work& wk) {
   __shared__ uint32_t s_win[2];
   const uint32_t cur = r % 3;
   uint32_t nb[NBIN];
@@ -230,7 +354,7 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
   }
   if (PUSH) {
     zero_plane(p, r);
-    phase_a_mask<S, CW>(p, bins, W, nb, wk);
+    phase_a_mask<S, POL, CW>(p, r, bins, W, nb, mark, wk);
   } else {
     phase_a_pull<S, CW>(p, bins, W, nb, wk, s_win);
   }
@@ -250,8 +374,8 @@ __device__ __forceinline__ void stv(void* p, const uint4& v) {
   asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-template <class S, bool CW>
-__device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work& wk) {
+template <class S, int POL, bool CW>
+__device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool mark, Work& wk) {
   S* st = (S*)p.st;
   reset_next(p, r);
   if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
@@ -264,10 +388,12 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work&
   const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
   const int64_t ngroups = ((int64_t)p.n + 15) / 16;
   const int64_t g0 = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31);
+  uint32_t nchg = 0;
+  int32_t* clist = bsmem().clist[threadIdx.x >> 5];
   for (int64_t gb = g0; gb < ngroups; gb += nthreads) {
     const int64_t g = gb + lane;
     const int64_t v0 = g * 16;
-    uint32_t fb = 0;
+    uint32_t fb = 0, chgm = 0;
     if (g < ngroups) {
       constexpr int NW = 4 * (int)sizeof(S);          // 32-bit words holding 16 state words
       constexpr int PER = 4 / (int)sizeof(S);          // state words per 32-bit word
@@ -293,10 +419,11 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work&
           const uint32_t t = b0 != 0xffu ? (uint32_t)__ffs(b0 ^ 0xffu) : plane_firstfit(p, (int32_t)(v0 + h));
           if (t == 0) {
             fb |= 1u << h;
-          } else {
+          } else if (t != (sv & SW<S>::CMASK)) {
             if (sizeof(S) == 1 && t > SW<S>::CMASK) atomicExch(&p.info->status, (uint32_t)ST_NEED16);
             w[wi] = (w[wi] & ~(SMASK << sh)) | ((t & SMASK) << sh);
             dirty = true;
+            chgm |= 1u << h;
           }
         }
       }
@@ -305,6 +432,49 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work&
         for (int i = 0; i < (int)sizeof(S); ++i)
           stv(st + v0 + i * (16 / sizeof(S)), make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
       }
+      nchg += __popc(chgm);
+    }
+    // marks of the changed vertices and their successors: the warp's changed vertices (up to
+    // 512, clustered along the colouring front) are listed in shared memory and dealt out one
+    // per lane per step; the successor ranges of a step are walked as one flattened loop
+    if (mark && __any_sync(FULL, chgm != 0)) {
+      const uint32_t c = __popc(chgm);
+      const uint32_t ci = warp_incl_scan(c, lane);
+      const uint32_t tot = __shfl_sync(FULL, ci, 31);
+      uint32_t at = ci - c;
+      for (uint32_t cm = chgm; cm; cm &= cm - 1) clist[at++] = (int32_t)(v0 + __ffs(cm) - 1);
+      __syncwarp();
+      for (uint32_t i0 = 0; i0 < tot; i0 += 32) {
+        int64_t lo = 0, hi = 0;
+        if (i0 + lane < tot) {
+          const int32_t v = clist[i0 + lane];
+          const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+          const int32_t k = POL != DEGREE ? ldks(p.ksplit + v) : 0;
+          lo = POL == HIGHER_ID ? beg + k : beg;
+          hi = POL == LOWER_ID ? beg + k : end;
+          sts(p.dirty + v, 1u);
+          if (CW) wk.v[W_MARK] += (unsigned long long)(hi - lo + 1);
+        }
+        const uint32_t Wn = (uint32_t)(hi - lo);
+        const uint32_t E = warp_incl_scan(Wn, lane);
+        const uint32_t T = __shfl_sync(FULL, E, 31);
+        for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
+          int32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t f = f0 + u * 32 + lane;
+            const int o = flat_owner(E, f);
+            const int oc = o < 32 ? o : 31;
+            const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+            const int64_t lo_o = __shfl_sync(FULL, lo, oc);
+            w[u] = f < T ? ldc(p.ci, lo_o + (f - (Eo - Wo))) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (w[u] >= 0) sts(p.dirty + w[u], 1u);
+        }
+      }
+      __syncwarp();
     }
     // colours beyond the planes: the whole warp, one vertex at a time (exact, reading C7)
     unsigned m = __ballot_sync(FULL, fb != 0);
@@ -319,10 +489,11 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, Work&
         const int32_t u = (int32_t)(sv0 + h);
         uint32_t t = 8u * p.np + 1u;
         if (sizeof(S) > 1 || t <= SW<S>::CMASK) t = firstfit_warp<S, CW>(p, u, t, wk, lane);
-        if (lane == 0) store_tent<S>(p, st, u, t);
+        if (lane == 0) tent_update<S, POL, CW>(p, st, u, t, lds(st + u) & SW<S>::CMASK, mark, -1, -1, -1, nchg, wk);
       }
     }
   }
+  flush_chg(p, r, nchg, wk, CW);
 }
 
 // ---------------------------------------------------------------- a3: Phase B + push
@@ -342,31 +513,6 @@ __device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, uint32_t ch, int lane
 // Position of the j-th entry of a scan range in scan order.
 __device__ __forceinline__ int64_t scan_pos(int64_t lo, int64_t hi, bool down, int64_t j) {
   return down ? hi - 1 - j : lo + j;
-}
-
-// ---- warp-flattened segment loops
-// Each lane of a warp holds a segment of W_i items (a vertex's next stretch of its conflict
-// scan, or a winner's row for the commit scatter).  The warp walks the concatenation of all
-// segments 32 x FLAT_U items per step, so short and long segments share the lanes evenly
-// instead of one lane (or one vertex at a time) doing all of a segment's work.  Item f
-// belongs to the lane `owner` with E[owner-1] <= f < E[owner] (E = inclusive prefix sum of
-// W over the lanes, found by a 5-step binary search over shuffles).
-constexpr int FLAT_U = 2;     // items per lane per step (independent loads in flight)
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
-__device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
-  int o = 0;
-#pragma unroll
-  for (int b = 16; b; b >>= 1)
-    if (__shfl_sync(FULL, E, o + b - 1) <= f) o += b;
-  return o;
 }
 
 // One batch of up to 32 vertices, one per lane (act).  The conflict scans of all of them
@@ -501,7 +647,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 // Sparse bin 0 (degree <= t3): warps pop chunks of the worklist; one vertex per lane.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
-                                             Work& wk, int* s_first) {
+                                             bool mark, Work& wk, int* s_first) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * WARPS;
@@ -510,7 +656,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
     const uint32_t cend = min(c0 + ch, cnt);
     for (uint32_t bse = c0; bse < cend; bse += 32) {
       const uint32_t i = bse + lane;
-      const bool act = i < cend;
+      bool act = i < cend, clean = false;
       WE e;
       e.v = 0;
       e.k = 0;
@@ -519,45 +665,27 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
       int64_t end = -1;
       if (act) {
         e = ldw(Wb + i);
+        if (mark) {
+          if (lds(p.dirty + e.v)) sts(p.dirty + e.v, 0u);
+          else clean = true;  // loses as it stands (N1)
+        }
+        act = !clean;
+      }
+      if (act) {
         tent = lds(st + e.v) & SW<S>::CMASK;
         if (e.k < 0 && POL != DEGREE) {
           end = RP(p, e.v + 1);
           e.k = row_split(p, e.v, e.beg, end);
         }
+        if (CW) wk.v[W_B_EVAL] += 1;
       }
-      const int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first);
+      int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first);
+      if (clean) state = 1;
       pu.template push<0, CW>(state == 1, e, lane, wk.v[W_PUSH]);
     }
   }
 }
 
-// Phase-B shared memory (one object per CTA, whichever phase function uses it).
-#ifndef GC_VPL
-#define GC_VPL 2
-#endif
-constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
-constexpr int WB = 32 * VPL;    // vertices per warp batch
-struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
-  int64_t sbase[WB];            // row position of scan step 0
-  uint32_t E[WB];               // inclusive prefix over the slots of the items of this pass
-  uint32_t pos[WB];             // scan steps done
-  int32_t k[WB];                // split (row start = sbase - k + 1 / sbase - k / sbase by policy)
-  uint32_t deg[WB];
-  int first[WB];                // work counters: first hit
-  uint32_t tent[WB];
-  uint32_t lost[VPL];
-};
-struct BSmem {
-  WE pbuf[WARPS][PBUF];   // per-warp push staging (Pusher, bin 0)
-  WideSeg seg[WARPS];     // dense batches
-  int first;              // conflict_cta
-  int32_t k;              // cta_vertex split broadcast
-  int cwfirst[WARPS][32]; // work counters: first hit per lane's vertex
-};
-__device__ __forceinline__ BSmem& bsmem() {
-  __shared__ BSmem s;
-  return s;
-}
 
 // One vertex of degree > t3 by the whole CTA (bin 1).  Returns true when it loses.
 template <class S, int POL, bool PUSH, bool CW>
@@ -585,7 +713,7 @@ __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent
 
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const WE* W, WE* Wout,
-                                        Work& wk) {
+                                        bool mark, Work& wk) {
   BSmem& sm = bsmem();
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
@@ -611,15 +739,26 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
     WE* Ob = Wout + bins.off[1];
     for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
       WE e = ldw(Wb + i);
-      const uint32_t tent = lds(st + e.v) & SW<S>::CMASK;
-      if (cta_vertex<S, POL, PUSH, CW>(p, e, tent, wk, &sm.first, &sm.k) && threadIdx.x == 0) {
+      if (threadIdx.x == 0) {  // one read of the state word and the dirty mark, broadcast
+        uint32_t x = lds(st + e.v) & SW<S>::CMASK;
+        if (mark) {
+          if (lds(p.dirty + e.v)) sts(p.dirty + e.v, 0u);
+          else x |= 0x40000000u;  // clean (N1)
+        }
+        sm.k = (int32_t)x;
+      }
+      __syncthreads();
+      const uint32_t tx = (uint32_t)sm.k;
+      __syncthreads();
+      if (CW && threadIdx.x == 0 && !(tx & 0x40000000u)) wk.v[W_B_EVAL] += 1;
+      if (((tx & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, tx, wk, &sm.first, &sm.k)) && threadIdx.x == 0) {
         stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
         if (CW) wk.v[W_PUSH] += 1;
       }
       __syncthreads();
     }
   }
-  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, wk, sm.cwfirst[warp]);
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, mark, wk, sm.cwfirst[warp]);
   pu.template flush<CW>(lane, wk.v[W_PUSH]);
 }
 
@@ -662,7 +801,7 @@ __device__ __forceinline__ uint32_t seg_len(const WideSeg& sg, int o) {
 
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t base, uint32_t cend, WideSeg& sg,
-                                             bool push_out, Pusher& pu, uint32_t& lost_cnt, Work& wk) {
+                                             bool push_out, bool mark, Pusher& pu, uint32_t& lost_cnt, Work& wk) {
   S* st = (S*)p.st;
   constexpr uint32_t CM = SW<S>::CMASK;
   constexpr int DIR = POL == HIGHER_ID ? -1 : 1;
@@ -679,11 +818,20 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     for (int h = 0; h <= VPL; ++h) rpv[h] = v0 + h <= cend ? ldr(p.rp, (int64_t)v0 + h) : 0;
 #pragma unroll
     for (int h = 0; h < VPL; ++h) kv[h] = (POL != DEGREE && v0 + h < cend) ? ldks(p.ksplit + v0 + h) : 0;
+    uint32_t dv[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) dv[h] = mark && v0 + h < cend ? lds(p.dirty + v0 + h) : 1u;
 #pragma unroll
     for (int h = 0; h < VPL; ++h) {
       const int sl = lane * VPL + h;
       const int64_t beg = rpv[h], deg = rpv[h + 1] - rpv[h];
-      const bool act = v0 + h < cend && !(sw[h] & SW<S>::COMMIT) && deg <= (int64_t)p.t3;
+      const bool pend = v0 + h < cend && !(sw[h] & SW<S>::COMMIT) && deg <= (int64_t)p.t3;
+      const bool act = pend && dv[h];
+      if (mark && pend) {
+        if (dv[h]) sts(p.dirty + v0 + h, 0u);
+        else states |= 1u << (8 * h);  // clean: loses as it stands (N1)
+      }
+      if (CW && act) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
       sg.sbase[sl] = POL == HIGHER_ID ? beg + kv[h] - 1 : (POL == LOWER_ID ? beg + kv[h] : beg);
       sg.k[sl] = kv[h];
       sg.deg[sl] = (uint32_t)deg;
@@ -870,7 +1018,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
 // that round r+1 runs sparse), pushed into W_out with the split already known.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const Bins& bins, WE* Wout, bool push_out,
-                                              Work& wk) {
+                                              bool mark, Work& wk) {
   BSmem& sm = bsmem();
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
@@ -891,12 +1039,21 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     WE* Ob = Wout + bins.off[1];
     for (uint32_t i = blockIdx.x; i < nh; i += gridDim.x) {
       WE e = ldw(p.heavy + i);
-      if (threadIdx.x == 0) sm.k = (int32_t)lds(st + e.v);  // one read, broadcast
+      if (threadIdx.x == 0) {  // one read of the state word and the dirty mark, broadcast
+        uint32_t x = lds(st + e.v);
+        if (mark && !(x & SW<S>::COMMIT)) {
+          if (lds(p.dirty + e.v)) sts(p.dirty + e.v, 0u);
+          else x |= 0x40000000u;  // clean (N1)
+        }
+        sm.k = (int32_t)x;
+      }
       __syncthreads();
       const uint32_t s = (uint32_t)sm.k;
       __syncthreads();
       if (s & SW<S>::COMMIT) continue;  // uniform over the CTA
-      if (cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k) && threadIdx.x == 0) {
+      if (CW && threadIdx.x == 0 && !(s & 0x40000000u)) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
+      if (((s & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k)) &&
+          threadIdx.x == 0) {
         if (push_out) {
           stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
           if (CW) wk.v[W_PUSH] += 1;
@@ -914,7 +1071,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < (uint32_t)p.n; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
     for (uint32_t bse = c0; bse < cend; bse += WB)
-      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, pu, lost_cnt, wk);
+      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk);
   }
   if (push_out) pu.template flush<CW>(lane, wk.v[W_PUSH]);
   else if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
@@ -987,9 +1144,15 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
   for (;;) {
     WE* Win = (WE*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
     WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
+    // dirty-set rounds (N1) on bounded-degree graphs with >= 4 successors per vertex on average
+    // (p.n1gain = min(m/2n, 8)): measured on B200, every round marks on the 27-point stencil
+    // (-11 %); marking costs more than it saves on the low-degree mesh (+8 %) and on R-MAT
+    // (hub rows: 2.4x slower when forced), and a per-round cost model based on the previous
+    // round's tentative-colour changes did no better than this rule
+    const bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && p.n1gain >= 4 && ld_relaxed(&p.info->maxdeg) <= 64u));
     if (r > 1) {
-      if (dense) phase_a_dense<S, CW>(p, r, wk);
-      else phase_a<S, PUSH, CW>(p, r, bins, Win, wk);
+      if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
+      else phase_a<S, POL, PUSH, CW>(p, r, bins, Win, mark, wk);
       if (!grid_sync(p)) return;
     }
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r - 1] = globaltimer();
@@ -997,10 +1160,10 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
       const uint32_t cur = r % 3;
       const uint64_t tot = (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
       const bool push_out = tot * p.dense_div <= (uint64_t)p.n;
-      phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, wk);
+      phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, mark, wk);
       if (push_out) dense = false;
     } else {
-      phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, wk);
+      phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, mark, wk);
     }
     if (!grid_sync(p)) return;
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
@@ -1034,7 +1197,7 @@ __global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, WE* W) 
   wk.zero();
   Bins b;
   b.load(p);
-  phase_a<uint32_t, PUSH, CW>(p, r, b, W, wk);
+  phase_a<uint32_t, HIGHER_ID, PUSH, CW>(p, r, b, W, false, wk);
   flush_work<CW>(p, wk);
 }
 template <int POL, bool PUSH, bool CW>
@@ -1043,7 +1206,7 @@ __global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, WE* W, 
   wk.zero();
   Bins b;
   b.load(p);
-  phase_b<uint32_t, POL, PUSH, CW>(p, r, b, W, Wout, wk);
+  phase_b<uint32_t, POL, PUSH, CW>(p, r, b, W, Wout, false, wk);
   flush_work<CW>(p, wk);
 }
 __global__ void __launch_bounds__(BLOCK) k_epilogue(Params p, uint32_t r) {
