@@ -90,7 +90,9 @@ typedef struct gc_work {
   uint64_t dense_b_evaluated;  /* of which in dense rounds */
   uint64_t dirty_marks;        /* dirty marks written (changed vertices and their successors) */
   uint64_t tent_changes;       /* tentative colours changed by Phase A */
-  uint64_t reserved[4];
+  uint64_t pending_degree_sum; /* sum over rounds r >= 2 of the degrees of the vertices in W_r
+                                  (round 1 adds m): the units of SURVEY §8(d)'s pull model */
+  uint64_t reserved[3];
 } gc_work;
 
 typedef struct gc_opts {

@@ -47,7 +47,8 @@ class Work(ctypes.Structure):
                 ("sparse_a_entries", ctypes.c_uint64), ("sparse_b_entries", ctypes.c_uint64),
                 ("state_bytes", ctypes.c_uint64), ("phase_b_evaluated", ctypes.c_uint64),
                 ("dense_b_evaluated", ctypes.c_uint64), ("dirty_marks", ctypes.c_uint64),
-                ("tent_changes", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 4)]
+                ("tent_changes", ctypes.c_uint64), ("pending_degree_sum", ctypes.c_uint64),
+                ("reserved", ctypes.c_uint64 * 3)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}

@@ -643,6 +643,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     o.work->dense_b_evaluated = hinfo.work[W_DB_EVAL];
     o.work->dirty_marks = hinfo.work[W_MARK];
     o.work->tent_changes = hinfo.work[W_TCHG];
+    o.work->pending_degree_sum = hinfo.work[W_WDEG];
   }
   *num_colors = hinfo.num_colors;
   *rounds = hinfo.rounds;

@@ -55,7 +55,7 @@ enum Policy { HIGHER_ID = 0, LOWER_ID = 1, DEGREE = 2 };
 constexpr int MAX_PLANES = 64;     // byte planes of forbidden colours: colours 1..512
 enum Status { ST_OK = 0, ST_NEED16 = 2, ST_NO_CONVERGENCE = 3, ST_NEED32 = 4, ST_WATCHDOG = 5 };
 enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_SCATTER_RED,
-               W_DA_SWEEP, W_DB_SWEEP, W_SA_ENT, W_SB_ENT, W_B_EVAL, W_DB_EVAL, W_MARK, W_TCHG, W_N };
+               W_DA_SWEEP, W_DB_SWEEP, W_SA_ENT, W_SB_ENT, W_B_EVAL, W_DB_EVAL, W_MARK, W_TCHG, W_WDEG, W_N };
 
 // State-word traits: top bit = committed, remaining bits = colour.
 template <class S> struct SW;

@@ -111,7 +111,10 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
 // instead of one lane (or one vertex at a time) doing all of a segment's work.  Item f
 // belongs to the lane `owner` with E[owner-1] <= f < E[owner] (E = inclusive prefix sum of
 // W over the lanes, found by a 5-step binary search over shuffles).
-constexpr int FLAT_U = 2;     // items per lane per step (independent loads in flight)
+#ifndef GC_FLAT_U
+#define GC_FLAT_U 2
+#endif
+constexpr int FLAT_U = GC_FLAT_U;  // items per lane per step (independent loads in flight)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 #pragma unroll
@@ -260,6 +263,7 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, uint32_t r, const 
       if (i < cnt) {
         e = ldw(Wb + i);
         t_old = lds(st + e.v) & SW<S>::CMASK;
+        if (CW) wk.v[W_WDEG] += (unsigned long long)(RP(p, e.v + 1) - e.beg);
         const uint32_t t = plane_firstfit(p, e.v);
         if (t) tent_update<S, POL, CW>(p, st, e.v, t, t_old, mark, e.beg, -1, e.k, nchg, wk);
         else fb = true;
@@ -409,6 +413,10 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
       }
       const uint4 pl = ldv(p.fmp + v0);
       const uint32_t pw[4] = {pl.x, pl.y, pl.z, pl.w};
+      // plane 1 as a vector too once colours 9.. can be committed (round >= 10)
+      uint4 pl1 = make_uint4(0, 0, 0, 0);
+      if (r >= 10 && p.np > 1) pl1 = ldv(p.fmp + p.plane + v0);
+      const uint32_t pw1[4] = {pl1.x, pl1.y, pl1.z, pl1.w};
       bool dirty = false;
 #pragma unroll
       for (int h = 0; h < 16; ++h) {
@@ -416,7 +424,10 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
         const uint32_t sv = (w[wi] >> sh) & SMASK;
         if (v0 + h < p.n && !(sv & SW<S>::COMMIT)) {
           const uint32_t b0 = (pw[h >> 2] >> ((h & 3) * 8)) & 0xffu;
-          const uint32_t t = b0 != 0xffu ? (uint32_t)__ffs(b0 ^ 0xffu) : plane_firstfit(p, (int32_t)(v0 + h));
+          const uint32_t b1 = (pw1[h >> 2] >> ((h & 3) * 8)) & 0xffu;
+          const uint32_t t = b0 != 0xffu   ? (uint32_t)__ffs(b0 ^ 0xffu)
+                             : b1 != 0xffu ? 8u + (uint32_t)__ffs(b1 ^ 0xffu)
+                                           : plane_firstfit(p, (int32_t)(v0 + h));
           if (t == 0) {
             fb |= 1u << h;
           } else if (t != (sv & SW<S>::CMASK)) {
@@ -433,6 +444,14 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           stv(st + v0 + i * (16 / sizeof(S)), make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
       }
       nchg += __popc(chgm);
+      if (CW) {  // sum of the degrees of the pending vertices (SURVEY §8(d) units)
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          const int wi = h / PER, sh = (h % PER) * 8 * (int)sizeof(S);
+          if (v0 + h < p.n && !(((w[wi] >> sh) & SMASK) & SW<S>::COMMIT))
+            wk.v[W_WDEG] += (unsigned long long)(ldr(p.rp, v0 + h + 1) - ldr(p.rp, v0 + h));
+        }
+      }
     }
     // marks of the changed vertices and their successors: the warp's changed vertices (up to
     // 512, clustered along the colouring front) are listed in shared memory and dealt out one
@@ -1065,10 +1084,11 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     }
   }
   const uint32_t nwarps = gridDim.x * WARPS;
-  const uint32_t ch = max((uint32_t)WB, min(2048u, ((uint32_t)p.n / (8u * nwarps)) / WB * WB));
+  const uint32_t nv = (uint32_t)p.n;
+  const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (8u * nwarps)) / WB * WB));
   uint32_t* q = &p.info->qctr[cur][0][0];
   uint32_t lost_cnt = 0;
-  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < (uint32_t)p.n; c0 = pop_chunk(q, ch, lane)) {
+  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nv; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
     for (uint32_t bse = c0; bse < cend; bse += WB)
       batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk);
