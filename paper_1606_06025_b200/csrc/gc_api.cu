@@ -356,7 +356,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
   if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
   const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 512;
-  void *ksplit = nullptr, *heavy = nullptr, *dirty = nullptr;
+  void *ksplit = nullptr, *heavy = nullptr, *dirty = nullptr, *wlw0 = nullptr, *wlw1 = nullptr, *dlist = nullptr;
+  uint32_t list_ok = 0;  // list rounds (GC_LIST: 0 off (default: slower on every config
+                         // measured), 1 cost rule, 2 from round 3 on)
+  if (const char* e = getenv("GC_LIST")) list_ok = (uint32_t)atoi(e);
   // dirty-set rounds: needs the per-vertex splits of the dense ingest
   uint32_t n1 = 1;
   if (const char* e = getenv("GC_N1")) n1 = (uint32_t)atoi(e);
@@ -369,6 +372,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     const int64_t hcap = m / ((int64_t)t3 + 1) + 1;  // vertices of degree > t3
     CK(sc.alloc(&ksplit, sizeof(int32_t) * (size_t)n));
     if (n1) CK(sc.alloc(&dirty, (size_t)pitch));
+    if (n1 && list_ok) {
+      CK(sc.alloc(&wlw0, sizeof(int32_t) * (size_t)n));
+      CK(sc.alloc(&wlw1, sizeof(int32_t) * (size_t)n));
+      CK(sc.alloc(&dlist, sizeof(int32_t) * (size_t)n));
+    }
     CK(sc.alloc(&heavy, sizeof(WE) * (size_t)(hcap < n ? hcap : n)));
   }
   CK(sc.alloc(&w0, sizeof(WE) * (size_t)n));
@@ -430,6 +438,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.dense_div = dense_div;
   p.ksplit = (int32_t*)ksplit;
   p.dirty = (uint8_t*)dirty;
+  p.wlw0 = (int32_t*)wlw0;
+  p.wlw1 = (int32_t*)wlw1;
+  p.dl = (int32_t*)dlist;
+  p.list_ok = dlist ? list_ok : 0u;
   p.n1 = dirty ? n1 : 0u;
   p.davg2 = n > 0 && m > 0 ? (uint32_t)((m + 2 * n - 1) / (2 * n)) + 1u : 1u;  // successors + 1
   p.n1gain = n > 0 ? (uint32_t)(m / (2 * n) < 8 ? m / (2 * n) : 8) : 0u;

@@ -79,7 +79,9 @@ struct DevInfo {
   uint32_t cursor[NBIN];
   uint32_t cnt[3][NBIN];        // |W| per bin, triple-buffered by round (r % 3)
   uint32_t chg[3];              // tentative colours changed by Phase A, by round (r % 3)
-  uint32_t pad1[5];
+  uint32_t wl_cnt[3];           // list rounds: winners recorded by Phase B, by round (r % 3)
+  uint32_t dl_cnt[3];           // list rounds: dirty vertices listed by Phase A, by round (r % 3)
+  uint32_t pad1[7];
   uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
   unsigned long long wlp[2];    // the two worklist buffers (re-read every round, see sgr_persistent)
   unsigned long long work[W_N];
@@ -115,6 +117,10 @@ struct Params {
   uint32_t dense_div;           // dense rounds while |W_r| * dense_div > n (0: always sparse)
   int32_t* ksplit;              // dense mode: number of lower-id neighbours of every vertex
   uint8_t* dirty;               // dirty-set rounds (N1): Phase B re-examines only marked vertices
+  int32_t* wlw0;                // list rounds: winners of even / odd rounds (capacity n each)
+  int32_t* wlw1;
+  int32_t* dl;                  // list rounds: the round's dirty vertices (capacity n)
+  uint32_t list_ok;             // list rounds allowed (GC_LIST)
   uint32_t n1;                  // dirty-set rounds enabled
   uint32_t davg2;               // average successors + 1 (m/2n + 1, rounded up): N1 cost model
   uint32_t n1gain;              // min(m/2n, 8): N1 saving per clean vertex, in units of marks

@@ -339,7 +339,11 @@ __device__ __forceinline__ void reset_next(const Params& p, uint32_t r) {
   if (blockIdx.x == 0 && threadIdx.x < NBIN) {
     p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
-    if (threadIdx.x == 0) p.info->chg[(r + 1) % 3] = 0;
+    if (threadIdx.x == 0) {
+      p.info->chg[(r + 1) % 3] = 0;
+      p.info->wl_cnt[(r + 1) % 3] = 0;
+      p.info->dl_cnt[(r + 1) % 3] = 0;
+    }
   }
 }
 
@@ -534,6 +538,17 @@ __device__ __forceinline__ int64_t scan_pos(int64_t lo, int64_t hi, bool down, i
   return down ? hi - 1 - j : lo + j;
 }
 
+// ---- list rounds: winners of round r recorded for Phase A of round r+1
+__device__ __forceinline__ void rec_winners(const Params& p, uint32_t r, bool win, int32_t v, int lane) {
+  const unsigned m = __ballot_sync(FULL, win);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
+  uint32_t pos = 0;
+  if (lane == leader) pos = atomicAdd(&p.info->wl_cnt[r % 3], (uint32_t)__popc(m));
+  pos = __shfl_sync(FULL, pos, leader);
+  if (win) ((r & 1) ? p.wlw1 : p.wlw0)[pos + __popc(m & lanemask_lt())] = v;
+}
+
 // One batch of up to 32 vertices, one per lane (act).  The conflict scans of all of them
 // advance together in passes over the flattened segments: pass 1 examines the first 4
 // positions of every scan range (the nearest lower ids, where most conflicts are), later
@@ -544,7 +559,7 @@ __device__ __forceinline__ int64_t scan_pos(int64_t lo, int64_t hi, bool down, i
 // when not yet read.  Returns the lane's state: 0 inactive, 1 lose, 2 win.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, const WE& e, uint32_t tent, int64_t end,
-                                       Work& wk, int* s_first) {
+                                       Work& wk, int* s_first, uint32_t rec_round = 0) {
   S* st = (S*)p.st;
   constexpr uint32_t CM = SW<S>::CMASK;
   int64_t sbase = 0, dv = 0;
@@ -620,6 +635,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
   // winners commit; the forbidden masks of their neighbours get their colour bit
   const bool win = state == 2;
   if (win) sts(st + e.v, tent | SW<S>::COMMIT);
+  if (rec_round) rec_winners(p, rec_round, win, e.v, lane);
   if (PUSH) {
     const bool sc = win && tent <= 8u * p.np;
     if (sc && end < 0) end = RP(p, e.v + 1);
@@ -666,7 +682,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 // Sparse bin 0 (degree <= t3): warps pop chunks of the worklist; one vertex per lane.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint32_t cnt, uint32_t* q, Pusher& pu,
-                                             bool mark, Work& wk, int* s_first) {
+                                             bool mark, Work& wk, int* s_first, uint32_t rec_round) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * WARPS;
@@ -698,7 +714,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
         }
         if (CW) wk.v[W_B_EVAL] += 1;
       }
-      int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first);
+      int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first, rec_round);
       if (clean) state = 1;
       pu.template push<0, CW>(state == 1, e, lane, wk.v[W_PUSH]);
     }
@@ -709,7 +725,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
 // One vertex of degree > t3 by the whole CTA (bin 1).  Returns true when it loses.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent, Work& wk, int* s_first,
-                                           int32_t* s_k) {
+                                           int32_t* s_k, uint32_t rec_round = 0) {
   S* st = (S*)p.st;
   const int64_t end = RP(p, e.v + 1);
   if (e.k < 0 && POL != DEGREE) {
@@ -721,7 +737,11 @@ __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent
   const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
   const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, s_first);
   if (!lose) {
-    if (threadIdx.x == 0) sts(st + e.v, tent | SW<S>::COMMIT);
+    if (threadIdx.x == 0) {
+      sts(st + e.v, tent | SW<S>::COMMIT);
+      if (rec_round)
+        (((rec_round & 1) ? p.wlw1 : p.wlw0))[atomicAdd(&p.info->wl_cnt[rec_round % 3], 1u)] = e.v;
+    }
     if (PUSH && tent <= 8u * p.np) {
       scatter<S, BLOCK, CW>(p, tent, e.beg + threadIdx.x, end, wk);
       if (CW && threadIdx.x == 0) wk.v[W_SCATTER] += (unsigned long long)(end - e.beg);
@@ -732,7 +752,8 @@ __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent
 
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins& bins, const WE* W, WE* Wout,
-                                        bool mark, Work& wk) {
+                                        bool mark, Work& wk, bool rec = false) {
+  const uint32_t rec_round = rec ? r : 0u;
   BSmem& sm = bsmem();
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
@@ -770,14 +791,16 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
       const uint32_t tx = (uint32_t)sm.k;
       __syncthreads();
       if (CW && threadIdx.x == 0 && !(tx & 0x40000000u)) wk.v[W_B_EVAL] += 1;
-      if (((tx & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, tx, wk, &sm.first, &sm.k)) && threadIdx.x == 0) {
+      if (((tx & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, tx, wk, &sm.first, &sm.k, rec_round)) &&
+          threadIdx.x == 0) {
         stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
         if (CW) wk.v[W_PUSH] += 1;
       }
       __syncthreads();
     }
   }
-  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, mark, wk, sm.cwfirst[warp]);
+  phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, mark, wk, sm.cwfirst[warp],
+                                 rec_round);
   pu.template flush<CW>(lane, wk.v[W_PUSH]);
 }
 
@@ -820,7 +843,8 @@ __device__ __forceinline__ uint32_t seg_len(const WideSeg& sg, int o) {
 
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t base, uint32_t cend, WideSeg& sg,
-                                             bool push_out, bool mark, Pusher& pu, uint32_t& lost_cnt, Work& wk) {
+                                             bool push_out, bool mark, Pusher& pu, uint32_t& lost_cnt, Work& wk,
+                                             uint32_t rec_round) {
   S* st = (S*)p.st;
   constexpr uint32_t CM = SW<S>::CMASK;
   constexpr int DIR = POL == HIGHER_ID ? -1 : 1;
@@ -970,6 +994,10 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
 #pragma unroll
   for (int h = 0; h < VPL; ++h)
     if (((states >> (8 * h)) & 0xffu) == 2u) sts(st + v0 + h, sg.tent[lane * VPL + h] | SW<S>::COMMIT);
+  if (rec_round) {
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) rec_winners(p, rec_round, ((states >> (8 * h)) & 0xffu) == 2u, (int32_t)(v0 + h), lane);
+  }
   // level 4: scatter of the winners' rows into the forbidden masks (flattened)
   if (PUSH) {
     uint32_t Wh[VPL];
@@ -1030,6 +1058,170 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
   __syncwarp();
 }
 
+// ---- list rounds (N1 with explicit lists; bounded-degree graphs, 8-bit state words)
+// Once few vertices commit per round, the dense sweeps cost more than the work: Phase A of
+// round r recomputes the tentative colour only of the neighbours of round r-1's winners (the
+// only masks that changed), and Phase B of round r examines only the vertices listed dirty by
+// that Phase A (the N1 rule above); every other pending vertex loses as it stands, so
+// |W_{r+1}| = |W_r| - (winners of round r).  Dirty marks are set with an atomic OR on the word
+// holding the mark byte, and the lane that set a mark lists the vertex (each listed once).
+__device__ __forceinline__ void mark_append(const Params& p, uint32_t r, bool act, int32_t v, int lane) {
+  bool nw = false;
+  if (act) {
+    const uint32_t sh = 8u * (uint32_t)(v & 3);
+    const uint32_t old = atomicOr((uint32_t*)(p.dirty + (v & ~3)), 1u << sh);
+    nw = ((old >> sh) & 0xffu) == 0u;
+  }
+  const unsigned m = __ballot_sync(FULL, nw);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
+  uint32_t pos = 0;
+  if (lane == leader) pos = atomicAdd(&p.info->dl_cnt[r % 3], (uint32_t)__popc(m));
+  pos = __shfl_sync(FULL, pos, leader);
+  if (nw) p.dl[pos + __popc(m & lanemask_lt())] = v;
+}
+
+// Marks (and lists) the cnt changed vertices of clist and their successors.
+template <int POL, bool CW>
+__device__ __forceinline__ void mark_flush(const Params& p, uint32_t r, const int32_t* clist, uint32_t cnt, int lane,
+                                           Work& wk) {
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const bool act = i0 + lane < cnt;
+    int32_t v = 0;
+    int64_t lo = 0, hi = 0;
+    if (act) {
+      v = clist[i0 + lane];
+      const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+      const int32_t k = POL != DEGREE ? ldks(p.ksplit + v) : 0;
+      lo = POL == HIGHER_ID ? beg + k : beg;
+      hi = POL == LOWER_ID ? beg + k : end;
+      if (CW) wk.v[W_MARK] += (unsigned long long)(hi - lo + 1);
+    }
+    mark_append(p, r, act, v, lane);
+    const uint32_t Wn = (uint32_t)(hi - lo);
+    const uint32_t E = warp_incl_scan(Wn, lane);
+    const uint32_t T = __shfl_sync(FULL, E, 31);
+    for (uint32_t f0 = 0; f0 < T; f0 += 32 * 2) {
+      int32_t w[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        const int o = flat_owner(E, f);
+        const int oc = o < 32 ? o : 31;
+        const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+        const int64_t lo_o = __shfl_sync(FULL, lo, oc);
+        w[u] = f < T ? ldc(p.ci, lo_o + (f - (Eo - Wo))) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) mark_append(p, r, w[u] >= 0, w[u], lane);
+    }
+  }
+}
+
+template <class S, int POL, bool CW>
+__device__ __forceinline__ void phase_a_list(const Params& p, uint32_t r, Work& wk) {
+  S* st = (S*)p.st;
+  reset_next(p, r);
+  zero_plane(p, r);
+  const int lane = threadIdx.x & 31;
+  int32_t* clist = bsmem().clist[threadIdx.x >> 5];
+  const uint32_t nwin = ld_relaxed(&p.info->wl_cnt[(r - 1) % 3]);
+  const int32_t* WL = ((r - 1) & 1) ? p.wlw1 : p.wlw0;
+  uint32_t* q = &p.info->qctr[r % 3][1][0];
+  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t ch = max(1u, min(32u, nwin / (4u * nwarps)));
+  uint32_t nchg = 0;
+  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nwin; c0 = pop_chunk(q, ch, lane)) {
+    const uint32_t cend = min(c0 + ch, nwin);
+    for (uint32_t bse = c0; bse < cend; bse += 32) {
+      int64_t lo = 0, hi = 0;
+      if (bse + lane < cend) {
+        const int32_t w = ldks(WL + bse + lane);
+        lo = ldr(p.rp, w);
+        hi = ldr(p.rp, w + 1);
+      }
+      const uint32_t Wn = (uint32_t)(hi - lo);
+      const uint32_t E = warp_incl_scan(Wn, lane);
+      const uint32_t T = __shfl_sync(FULL, E, 31);
+      for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
+        int32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t f = f0 + u * 32 + lane;
+          const int o = flat_owner(E, f);
+          const int oc = o < 32 ? o : 31;
+          const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
+          const int64_t lo_o = __shfl_sync(FULL, lo, oc);
+          v[u] = f < T ? ldc(p.ci, lo_o + (f - (Eo - Wo))) : -1;
+        }
+        uint32_t sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sv[u] = v[u] >= 0 ? lds(st + v[u]) : SW<S>::COMMIT;
+        uint32_t chm = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (sv[u] & SW<S>::COMMIT) continue;
+          const uint32_t t = plane_firstfit(p, v[u]);  // >= 1: 8-bit words, colours <= 8 * np
+          if (t != (sv[u] & SW<S>::CMASK)) {
+            store_tent<S>(p, st, v[u], t);
+            chm |= 1u << u;
+          }
+        }
+        // list this step's changed vertices (<= 128) and mark them with their successors
+        const uint32_t c = __popc(chm);
+        nchg += c;
+        const uint32_t ci = warp_incl_scan(c, lane);
+        const uint32_t tot = __shfl_sync(FULL, ci, 31);
+        if (tot) {
+          uint32_t at = ci - c;
+          for (uint32_t m = chm; m; m &= m - 1) clist[at++] = v[__ffs(m) - 1];
+          __syncwarp();
+          mark_flush<POL, CW>(p, r, clist, tot, lane, wk);
+          __syncwarp();
+        }
+      }
+    }
+  }
+  flush_chg(p, r, nchg, wk, CW);
+}
+
+template <class S, int POL, bool PUSH, bool CW>
+__device__ __forceinline__ void phase_b_list(const Params& p, uint32_t r, uint32_t tot, Work& wk) {
+  S* st = (S*)p.st;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
+    if (CW) wk.v[W_B_VERT] += tot;
+  }
+  const uint32_t nd = ld_relaxed(&p.info->dl_cnt[r % 3]);
+  uint32_t* q = &p.info->qctr[r % 3][0][0];
+  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t ch = max(1u, min(64u, nd / (4u * nwarps)));
+  int* s_first = bsmem().cwfirst[warp];
+  for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nd; c0 = pop_chunk(q, ch, lane)) {
+    const uint32_t cend = min(c0 + ch, nd);
+    for (uint32_t bse = c0; bse < cend; bse += 32) {
+      bool act = bse + lane < cend;
+      WE e;
+      e.v = 0;
+      e.k = 0;
+      e.beg = 0;
+      uint32_t tent = 0;
+      if (act) {
+        e.v = ldks(p.dl + bse + lane);
+        sts(p.dirty + e.v, 0u);
+        const uint32_t sv = lds(st + e.v);
+        act = !(sv & SW<S>::COMMIT);
+        tent = sv & SW<S>::CMASK;
+        e.beg = ldr(p.rp, e.v);
+        if (POL != DEGREE) e.k = ldks(p.ksplit + e.v);
+        if (CW && act) wk.v[W_B_EVAL] += 1;
+      }
+      batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, -1, wk, s_first, r);
+    }
+  }
+}
+
 // Dense Phase B: W_r = all uncommitted vertices.  The heavy vertices (degree > t3, a static
 // list built by the ingest) are taken one CTA each; the others by warps popping chunks of
 // consecutive ids (coalesced state words, row offsets and splits; consecutive rows are
@@ -1037,7 +1229,8 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
 // that round r+1 runs sparse), pushed into W_out with the split already known.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const Bins& bins, WE* Wout, bool push_out,
-                                              bool mark, Work& wk) {
+                                              bool mark, Work& wk, bool rec = false) {
+  const uint32_t rec_round = rec ? r : 0u;
   BSmem& sm = bsmem();
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
@@ -1071,7 +1264,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       __syncthreads();
       if (s & SW<S>::COMMIT) continue;  // uniform over the CTA
       if (CW && threadIdx.x == 0 && !(s & 0x40000000u)) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
-      if (((s & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k)) &&
+      if (((s & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k, rec_round)) &&
           threadIdx.x == 0) {
         if (push_out) {
           stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
@@ -1085,13 +1278,87 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   }
   const uint32_t nwarps = gridDim.x * WARPS;
   const uint32_t nv = (uint32_t)p.n;
-  const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (8u * nwarps)) / WB * WB));
   uint32_t* q = &p.info->qctr[cur][0][0];
   uint32_t lost_cnt = 0;
+  if (mark && !push_out) {
+    // dirty-set round: sweep the marks and state words 512 vertices per warp step (16-B
+    // vectors), list the dirty pending ones in shared memory and examine only those, 32 per
+    // batch (one per lane); clean pending vertices lose as they stand
+    int32_t* clist = sm.clist[warp];
+    int* s_first = sm.cwfirst[warp];
+    constexpr uint32_t CHD = 512;
+    for (uint32_t c0 = pop_chunk(q, CHD, lane); c0 < nv; c0 = pop_chunk(q, CHD, lane)) {
+      const uint32_t v0 = c0 + 16u * lane;
+      uint32_t cand = 0, pend = 0;
+      if (v0 < nv) {
+        const uint4 dq = ldv(p.dirty + v0);
+        const uint32_t dw[4] = {dq.x, dq.y, dq.z, dq.w};
+        uint32_t sw[4 * sizeof(S)];
+#pragma unroll
+        for (int i = 0; i < (int)sizeof(S); ++i) {
+          const uint4 x = ldv(st + v0 + i * (16 / sizeof(S)));
+          sw[4 * i] = x.x;
+          sw[4 * i + 1] = x.y;
+          sw[4 * i + 2] = x.z;
+          sw[4 * i + 3] = x.w;
+        }
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          constexpr int PER = 4 / (int)sizeof(S);
+          const uint32_t sv = sw[h / PER] >> ((h % PER) * 8 * (int)sizeof(S));
+          const bool pd = v0 + h < nv && !(sv & SW<S>::COMMIT);
+          pend |= (uint32_t)pd << h;
+          cand |= (uint32_t)(pd && ((dw[h >> 2] >> ((h & 3) * 8)) & 0xffu)) << h;
+        }
+      }
+      const uint32_t c = __popc(cand);
+      const uint32_t ci = warp_incl_scan(c, lane);
+      const uint32_t tot = __shfl_sync(FULL, ci, 31);
+      uint32_t at = ci - c;
+      for (uint32_t m = cand; m; m &= m - 1) clist[at++] = (int32_t)(v0 + __ffs(m) - 1);
+      __syncwarp();
+      uint32_t won = 0;
+      for (uint32_t i0 = 0; i0 < tot; i0 += 32) {
+        bool act = i0 + lane < tot;
+        WE e;
+        e.v = 0;
+        e.k = 0;
+        e.beg = 0;
+        uint32_t tent = 0;
+        int64_t end = -1;
+        if (act) {
+          e.v = clist[i0 + lane];
+          tent = lds(st + e.v) & SW<S>::CMASK;
+          e.beg = ldr(p.rp, e.v);
+          end = ldr(p.rp, e.v + 1);
+          if (POL != DEGREE) e.k = ldks(p.ksplit + e.v);
+          act = end - e.beg <= (int64_t)p.t3;  // heavy vertices (and their marks): the CTA loop
+          if (act) sts(p.dirty + e.v, 0u);
+          if (CW && act) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
+        }
+        const int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first, rec_round);
+        won += __popc(__ballot_sync(FULL, state == 2));
+      }
+      __syncwarp();
+      // heavy pending vertices are counted by the CTA loop
+      uint32_t heavy_pend = 0;
+      if (bins.size[1]) {
+        for (uint32_t m = pend; m; m &= m - 1) {
+          const int32_t v = (int32_t)(v0 + __ffs(m) - 1);
+          if (ldr(p.rp, v + 1) - ldr(p.rp, v) > (int64_t)p.t3) ++heavy_pend;
+        }
+      }
+      const uint32_t np = __reduce_add_sync(FULL, (uint32_t)__popc(pend) - heavy_pend);
+      lost_cnt += np - won;
+    }
+    if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
+    return;
+  }
+  const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (8u * nwarps)) / WB * WB));
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nv; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
     for (uint32_t bse = c0; bse < cend; bse += WB)
-      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk);
+      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk, rec_round);
   }
   if (push_out) pu.template flush<CW>(lane, wk.v[W_PUSH]);
   else if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
@@ -1160,10 +1427,15 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
   // Rounds run dense (W_r implicit, id-order sweeps) while |W_r| * dense_div > n, then
   // sparse (worklists); the round whose |W_r| first falls below pushes its losers.
   uint32_t r = 1;
-  bool dense = dense0;
+  bool dense = dense0, list = false;
+  uint32_t tot_list = 0;
+  // list rounds: 8-bit words (colours from the planes), bounded degree, dirty marks available
+  const bool can_list = sizeof(S) == 1 && PUSH && p.list_ok && p.dirty && ld_relaxed(&p.info->maxdeg) <= 64u;
   for (;;) {
     WE* Win = (WE*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
     WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
+    const uint32_t cur = r % 3;
+    const uint64_t tot = list ? tot_list : (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
     // dirty-set rounds (N1) on bounded-degree graphs with >= 4 successors per vertex on average
     // (p.n1gain = min(m/2n, 8)): measured on B200, every round marks on the 27-point stencil
     // (-11 %); marking costs more than it saves on the low-degree mesh (+8 %) and on R-MAT
@@ -1171,23 +1443,38 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
     // round's tentative-colour changes did no better than this rule
     const bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && p.n1gain >= 4 && ld_relaxed(&p.info->maxdeg) <= 64u));
     if (r > 1) {
-      if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
+      if (list) phase_a_list<S, POL, CW>(p, r, wk);
+      else if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
       else phase_a<S, POL, PUSH, CW>(p, r, bins, Win, mark, wk);
       if (!grid_sync(p)) return;
     }
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r - 1] = globaltimer();
-    if (dense) {
-      const uint32_t cur = r % 3;
-      const uint64_t tot = (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
-      const bool push_out = tot * p.dense_div <= (uint64_t)p.n;
-      phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, mark, wk);
+    // round r+1 runs as a list round when round r-1's winners x 4 (successors + 1) <= n
+    // (p.list_ok == 2: from round 2 on, tests); round r then records its winners
+    bool list_next = list;
+    if (!list && can_list && r >= 2) {
+      const uint64_t prev = (uint64_t)ld_relaxed(&p.info->cnt[(r - 1) % 3][0]) + ld_relaxed(&p.info->cnt[(r - 1) % 3][1]);
+      const uint64_t won = prev > tot ? prev - tot : 0;
+      list_next = p.list_ok == 2 || won * 4 * p.davg2 <= (uint64_t)p.n;
+    }
+    if (list) {
+      phase_b_list<S, POL, PUSH, CW>(p, r, (uint32_t)tot, wk);
+    } else if (dense) {
+      const bool push_out = !list_next && tot * p.dense_div <= (uint64_t)p.n;
+      phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, mark, wk, list_next);
       if (push_out) dense = false;
     } else {
-      phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, mark, wk);
+      phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, mark, wk, list_next);
     }
     if (!grid_sync(p)) return;
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
-    const uint32_t left = next_total(p, r);
+    uint32_t left;
+    if (list) left = (uint32_t)tot - ld_relaxed(&p.info->wl_cnt[cur]);
+    else left = next_total(p, r);
+    if (list_next) {
+      list = true;
+      tot_list = left;
+    }
     if (left == 0) break;
     if (r >= p.max_rounds) {
       if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&p.info->status, (uint32_t)ST_NO_CONVERGENCE);

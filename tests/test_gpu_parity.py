@@ -90,7 +90,8 @@ def test_parity_variants(gc, kw):
                                  dict(GC_DENSE_DIV="0"), dict(GC_DENSE_DIV="1"),
                                  dict(GC_DENSE_DIV="1000000000"), dict(GC_N1="0"), dict(GC_N1="2"),
                                  dict(GC_N1="2", GC_DENSE_DIV="1"), dict(GC_N1="2", GC_DENSE_DIV="1000000000"),
-                                 dict(GC_N1="2", GC_STATE_BYTES="2")],
+                                 dict(GC_N1="2", GC_STATE_BYTES="2"), dict(GC_LIST="0"), dict(GC_LIST="2"),
+                                 dict(GC_LIST="2", GC_N1="2"), dict(GC_LIST="2", GC_DENSE_DIV="1")],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_parity_env_variants(gc, env, monkeypatch):
     """Forced state-word widths, filtered commit scatter, no L2 window: same result."""
@@ -103,6 +104,20 @@ def test_parity_env_variants(gc, env, monkeypatch):
             _check(gc, g, pol)
             _check(gc, g, pol, warp_bin_max=8)
         _check(gc, g, "higher_id", host_rounds=True)
+
+
+@pytest.mark.parametrize("env", [dict(GC_LIST="2"), dict(GC_LIST="2", GC_N1="2"), dict(GC_LIST="2", GC_DENSE_DIV="1"),
+                                 dict(GC_LIST="2", GC_DENSE_DIV="0"), dict(GC_LIST="1")],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_parity_list_rounds(gc, env, monkeypatch):
+    """List rounds (bounded degree <= 64, 8-bit words): entered from dense, sparse or switch rounds."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for g in (wl.mesh2d(100, 77, 0.3), wl.mesh2d(64, 64), wl.stencil27(9, 7, 5), wl.stencil27(12),
+              wl.gnp(400, 0.02, 3), wl.path(1000), wl.cycle(999), wl.rmat(12, 2, wl.RMAT_ER)):
+        assert g.max_degree() <= 64
+        for pol in POLICIES:
+            _check(gc, g, pol)
 
 
 @pytest.mark.parametrize("k", [126, 127, 128, 129, 136])
