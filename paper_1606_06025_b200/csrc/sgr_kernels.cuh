@@ -1436,12 +1436,11 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
     WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
     const uint32_t cur = r % 3;
     const uint64_t tot = list ? tot_list : (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
-    // dirty-set rounds (N1) on bounded-degree graphs with >= 4 successors per vertex on average
-    // (p.n1gain = min(m/2n, 8)): measured on B200, every round marks on the 27-point stencil
-    // (-11 %); marking costs more than it saves on the low-degree mesh (+8 %) and on R-MAT
-    // (hub rows: 2.4x slower when forced), and a per-round cost model based on the previous
-    // round's tentative-colour changes did no better than this rule
-    const bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && p.n1gain >= 4 && ld_relaxed(&p.info->maxdeg) <= 64u));
+    // dirty-set rounds (N1) on bounded-degree graphs (max degree <= 64): measured on B200, every
+    // round marks on the 27-point stencil (-22 %) and the mesh (-4 %); on R-MAT marking the
+    // hub rows costs more than it saves (2.4x slower when forced), and a per-round cost model
+    // based on the previous round's tentative-colour changes did no better than this rule
+    const bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && ld_relaxed(&p.info->maxdeg) <= 64u));
     if (r > 1) {
       if (list) phase_a_list<S, POL, CW>(p, r, wk);
       else if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
@@ -1460,7 +1459,8 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
     if (list) {
       phase_b_list<S, POL, PUSH, CW>(p, r, (uint32_t)tot, wk);
     } else if (dense) {
-      const bool push_out = !list_next && tot * p.dense_div <= (uint64_t)p.n;
+      // dirty-set rounds make the dense sweep cheap for clean vertices: stay dense longer
+      const bool push_out = !list_next && tot * (mark ? p.dense_div_n1 : p.dense_div) <= (uint64_t)p.n;
       phase_b_dense<S, POL, PUSH, CW>(p, r, bins, Wout, push_out, mark, wk, list_next);
       if (push_out) dense = false;
     } else {
