@@ -44,7 +44,10 @@
 namespace gcdev {
 
 constexpr int NBIN = 2;            // 0 = thread probe + warp continuation, 1 = CTA per vertex
-constexpr int PROBE = 4;           // Phase-B positions a vertex's own thread examines first
+#ifndef GC_PROBE
+#define GC_PROBE 4
+#endif
+constexpr int PROBE = GC_PROBE;    // Phase-B positions a vertex's own thread examines first
 constexpr int PBUF = 64;           // per-warp push staging entries per bin
 constexpr int BLOCK = 256;
 constexpr int WARPS = BLOCK / 32;
@@ -116,6 +119,7 @@ struct Params {
   uint32_t sfilter;             // commit scatter skips neighbours already committed
   uint32_t dense_div;           // dense rounds while |W_r| * dense_div > n (0: always sparse)
   uint32_t dense_div_n1;        // the same in dirty-set rounds
+  uint32_t compact;             // dense Phase B lists the pending vertices (also without marks)
   int32_t* ksplit;              // dense mode: number of lower-id neighbours of every vertex
   uint8_t* dirty;               // dirty-set rounds (N1): Phase B re-examines only marked vertices
   int32_t* wlw0;                // list rounds: winners of even / odd rounds (capacity n each)

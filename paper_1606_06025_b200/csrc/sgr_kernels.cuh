@@ -576,7 +576,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     state = len ? 3 : 2;
   }
   // conflict-scan passes
-  uint32_t cap = 4;
+  uint32_t cap = PROBE;
   for (;;) {
     const bool und = state == 3;
     if (!__any_sync(FULL, und)) break;
@@ -630,7 +630,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         }
       }
     }
-    cap = cap < 1024 ? cap * 4 - (cap == 4 ? 4 : 0) : cap;  // 4, 12, 48, 192, 768, ...
+    cap = cap < 1024 ? (cap == (uint32_t)PROBE ? 3 * PROBE : cap * 4) : cap;  // 4, 12, 48, 192, 768, ...
   }
   // winners commit; the forbidden masks of their neighbours get their colour bit
   const bool win = state == 2;
@@ -725,7 +725,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
 // One vertex of degree > t3 by the whole CTA (bin 1).  Returns true when it loses.
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent, Work& wk, int* s_first,
-                                           int32_t* s_k, uint32_t rec_round = 0) {
+                                           int32_t* s_k, uint32_t rec_round = 0, bool first_round = false) {
   S* st = (S*)p.st;
   const int64_t end = RP(p, e.v + 1);
   if (e.k < 0 && POL != DEGREE) {
@@ -735,7 +735,9 @@ __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent
     __syncthreads();
   }
   const ScanRange<POL> sr = scan_range<POL>(e.beg, e.k, end);
-  const bool lose = conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down, end - e.beg, wk, s_first);
+  const bool lose = (POL != DEGREE && first_round) ? sr.hi > sr.lo  // round 1: see batch_b_wide
+                                                  : conflict_cta<S, POL, CW>(p, e.v, tent, sr.lo, sr.hi, sr.down,
+                                                                             end - e.beg, wk, s_first);
   if (!lose) {
     if (threadIdx.x == 0) {
       sts(st + e.v, tent | SW<S>::COMMIT);
@@ -844,7 +846,7 @@ __device__ __forceinline__ uint32_t seg_len(const WideSeg& sg, int o) {
 template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t base, uint32_t cend, WideSeg& sg,
                                              bool push_out, bool mark, Pusher& pu, uint32_t& lost_cnt, Work& wk,
-                                             uint32_t rec_round) {
+                                             uint32_t rec_round, bool first_round) {
   S* st = (S*)p.st;
   constexpr uint32_t CM = SW<S>::CMASK;
   constexpr int DIR = POL == HIGHER_ID ? -1 : 1;
@@ -887,6 +889,17 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     }
   }
   __syncwarp();
+  // round 1: every vertex is pending with tentative colour 1, so (id policies) a vertex loses
+  // iff its scan range is not empty — no gathers (same result as the scan: its first position
+  // conflicts)
+  if (POL != DEGREE && first_round) {
+#pragma unroll
+    for (int h = 0; h < VPL; ++h)
+      if (((states >> (8 * h)) & 0xffu) == 3u) {
+        states ^= 2u << (8 * h);  // 3 -> 1
+        if (CW) { wk.v[W_B_EDGE] += 1; wk.v[W_B_GATHER] += 1; }
+      }
+  }
   // pass 1, lane-local: the first PROBE positions of the lane's own VPL scan ranges (no owner
   // search; VPL x PROBE independent loads per lane).  Later passes are flattened.
   {
@@ -927,7 +940,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     __syncwarp();
   }
   // conflict-scan passes (levels 2-3: col_idx of the scan positions, then their state words)
-  uint32_t cap = 12;
+  uint32_t cap = 3 * PROBE;
   for (;;) {
     const bool any = ((states | states >> 1) & 0x01010101u & (states & (states >> 1))) != 0;  // some slot == 3
     if (!__any_sync(FULL, any)) break;
@@ -1264,7 +1277,8 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       __syncthreads();
       if (s & SW<S>::COMMIT) continue;  // uniform over the CTA
       if (CW && threadIdx.x == 0 && !(s & 0x40000000u)) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
-      if (((s & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k, rec_round)) &&
+      if (((s & 0x40000000u) ||
+           cta_vertex<S, POL, PUSH, CW>(p, e, s & SW<S>::CMASK, wk, &sm.first, &sm.k, rec_round, r == 1)) &&
           threadIdx.x == 0) {
         if (push_out) {
           stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
@@ -1280,7 +1294,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   const uint32_t nv = (uint32_t)p.n;
   uint32_t* q = &p.info->qctr[cur][0][0];
   uint32_t lost_cnt = 0;
-  if (mark && !push_out) {
+  if ((mark || p.compact) && !push_out) {
     // dirty-set round: sweep the marks and state words 512 vertices per warp step (16-B
     // vectors), list the dirty pending ones in shared memory and examine only those, 32 per
     // batch (one per lane); clean pending vertices lose as they stand
@@ -1291,7 +1305,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       const uint32_t v0 = c0 + 16u * lane;
       uint32_t cand = 0, pend = 0;
       if (v0 < nv) {
-        const uint4 dq = ldv(p.dirty + v0);
+        const uint4 dq = mark ? ldv(p.dirty + v0) : make_uint4(0, 0, 0, 0);
         const uint32_t dw[4] = {dq.x, dq.y, dq.z, dq.w};
         uint32_t sw[4 * sizeof(S)];
 #pragma unroll
@@ -1308,7 +1322,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
           const uint32_t sv = sw[h / PER] >> ((h % PER) * 8 * (int)sizeof(S));
           const bool pd = v0 + h < nv && !(sv & SW<S>::COMMIT);
           pend |= (uint32_t)pd << h;
-          cand |= (uint32_t)(pd && ((dw[h >> 2] >> ((h & 3) * 8)) & 0xffu)) << h;
+          cand |= (uint32_t)(pd && (!mark || ((dw[h >> 2] >> ((h & 3) * 8)) & 0xffu))) << h;
         }
       }
       const uint32_t c = __popc(cand);
@@ -1333,7 +1347,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
           end = ldr(p.rp, e.v + 1);
           if (POL != DEGREE) e.k = ldks(p.ksplit + e.v);
           act = end - e.beg <= (int64_t)p.t3;  // heavy vertices (and their marks): the CTA loop
-          if (act) sts(p.dirty + e.v, 0u);
+          if (act && mark) sts(p.dirty + e.v, 0u);
           if (CW && act) wk.v[W_B_EVAL] += 1, wk.v[W_DB_EVAL] += 1;
         }
         const int state = batch_b<S, POL, PUSH, CW>(p, lane, act, e, tent, end, wk, s_first, rec_round);
@@ -1358,7 +1372,8 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nv; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
     for (uint32_t bse = c0; bse < cend; bse += WB)
-      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk, rec_round);
+      batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk, rec_round,
+                                     r == 1);
   }
   if (push_out) pu.template flush<CW>(lane, wk.v[W_PUSH]);
   else if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);

@@ -43,6 +43,8 @@ def main():
     variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
                          dict(host_rounds=True, pull_firstfit=True)]
     variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
+    variants["compact"] = [dict(), dict(env={"GC_COMPACT": "1"}), dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "16"}),
+                           dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "64"})]
     variants["list"] = [dict(env={"GC_LIST": x}) for x in ("0", "1", "2")]
     variants["n1"] = [dict(env={"GC_N1": x}) for x in ("0", "1", "2")]
     variants["dense"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("0", "2", "4", "8", "16", "64")]
