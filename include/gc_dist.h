@@ -19,7 +19,12 @@
  *   finalize; destroy
  *
  * Round r reads exactly the state the single-GPU path reads (Jacobi rounds, reading C2), so
- * the colours are bit-identical to gc_color for every cover of [0, n).  Policies HIGHER_ID
+ * the colours are bit-identical to gc_color for every cover of [0, n).
+ * First-Fit is incremental as on one GPU: each partition keeps forbidden-colour planes for its
+ * own vertices; local winners OR their colour into them directly, and the commit pairs of
+ * remote winners are applied through a halo adjacency (for every remote vertex, its local
+ * neighbours) built by gc_dist_create.  Only boundary vertices (with a remote neighbour) are
+ * packed: no other partition ever reads the others' words.  Policies HIGHER_ID
  * and LOWER_ID (global ids decide); DEGREE is single-GPU only (GC_ERR_UNSUPPORTED).
  * All pointers are device memory of opts->device; every call is synchronous on the
  * partition's internal stream.  Errors: see gc.h conventions.
@@ -34,7 +39,8 @@ extern "C" {
 
 typedef struct gc_dist gc_dist;
 
-/* Allocate the partition state (replicated state words: 4 B x n_global) and build W_1. */
+/* Allocate the partition state (replicated state words: 4 B x n_global; forbidden-colour
+ * planes; halo adjacency, 4 B per cut edge) from the device's stream-ordered pool and build W_1. */
 gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64_t v_end,
                          const int64_t* row_ptr_local, const int32_t* col_idx_local,
                          const gc_opts* opts);
@@ -42,10 +48,12 @@ gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64
 gc_status gc_dist_phase_a(gc_dist* h);
 /* Phase B (ConflictResolve + push); *local_next = local |W_{r+1}|. */
 gc_status gc_dist_phase_b(gc_dist* h, uint32_t* local_next);
-/* what 0: (v, word) of the local pending vertices (after Phase A); what 1: the local winners
- * (after Phase B).  pairs: device, >= 2*(v_end-v_begin) uint32; *count = pairs written. */
+/* what 0: (v, word) of the local pending boundary vertices (after Phase A); what 1: the local
+ * boundary winners (after Phase B).  pairs: device, >= 2*(v_end-v_begin) uint32; *count =
+ * pairs written. */
 gc_status gc_dist_pack(gc_dist* h, int32_t what, uint32_t* pairs, uint64_t* count);
-/* Write gathered (v, word) pairs into the replicated state. */
+/* Write gathered (v, word) pairs into the replicated state; committed words of remote
+ * vertices also set their colour bit in the planes of their local neighbours (halo). */
 gc_status gc_dist_unpack(gc_dist* h, const uint32_t* pairs, uint64_t count);
 /* W_{r+1} becomes the input worklist of round r+1. */
 gc_status gc_dist_next_round(gc_dist* h);

@@ -13,6 +13,7 @@
 // Every partition therefore sees exactly the single-GPU state after each phase, so the
 // colouring is bit-identical to one GPU for any cover of [0, n).
 #pragma once
+#include <cub/device/device_scan.cuh>
 
 namespace gcdev {
 
@@ -24,7 +25,8 @@ __global__ void __launch_bounds__(BLOCK) k_fill_u32(uint32_t* p, int64_t n, uint
 // entries whose word has the commit bit (this round's winners).
 __global__ void __launch_bounds__(BLOCK) k_pack(const WE* W, const uint32_t* off, const uint32_t* cnt,
                                                 const uint32_t* st, int only_committed, uint32_t* out,
-                                                unsigned long long* out_count) {
+                                                unsigned long long* out_count, const uint8_t* boundary,
+                                                int32_t v_base) {
   const int lane = threadIdx.x & 31;
   for (int b = 0; b < NBIN; ++b) {
     const uint32_t nb = cnt[b];
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(BLOCK) k_pack(const WE* W, const uint32_t* off
       if (i < nb) {
         v = ldw_v(Wb + i);
         s = lds(st + v);
-        take = !only_committed || (s & SW<uint32_t>::COMMIT);
+        take = boundary[v - v_base] && (!only_committed || (s & SW<uint32_t>::COMMIT));
       }
       const unsigned m = __ballot_sync(FULL, take);
       if (!m) continue;
@@ -58,6 +60,55 @@ __global__ void __launch_bounds__(BLOCK) k_unpack(const uint32_t* pairs, int64_t
     st[pairs[2 * i]] = pairs[2 * i + 1];
 }
 
+// Halo adjacency (push First-Fit across partitions): for every remote vertex w, the local
+// vertices adjacent to it (the symmetric half of the cut edges), as offsets hoff[w] into hadj.
+// A remote winner's colour bit reaches the forbidden-colour planes of its local neighbours
+// through this list when its commit pair is unpacked (the winner's own partition cannot RED
+// into another GPU's planes).
+// One warp per local vertex (coalesced row reads; hub rows do not serialise one thread).
+__global__ void __launch_bounds__(BLOCK) k_halo_count(Params p, int64_t n_local, int64_t v_begin, int64_t v_end,
+                                                      uint32_t* hcnt, uint8_t* boundary) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * BLOCK) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < n_local; u += nw) {
+    bool b = false;
+    for (int64_t e = p.rp[u] + lane; e < p.rp[u + 1]; e += 32) {
+      const int32_t w = p.ci[e];
+      if (w < v_begin || w >= v_end) {
+        atomicAdd(&hcnt[w], 1u);
+        b = true;
+      }
+    }
+    b = __any_sync(FULL, b);
+    if (lane == 0) boundary[u] = b ? 1 : 0;  // only boundary vertices' words are read remotely
+  }
+}
+__global__ void __launch_bounds__(BLOCK) k_halo_fill(Params p, int64_t n_local, int64_t v_begin, int64_t v_end,
+                                                     uint32_t* hcur, int32_t* hadj) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * BLOCK) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < n_local; u += nw)
+    for (int64_t e = p.rp[u] + lane; e < p.rp[u + 1]; e += 32) {
+      const int32_t w = p.ci[e];
+      if (w < v_begin || w >= v_end) hadj[atomicAdd(&hcur[w], 1u)] = (int32_t)(v_begin + u);
+    }
+}
+// Commit pairs of remote winners -> colour bit into the planes of their local neighbours.
+__global__ void __launch_bounds__(BLOCK) k_halo_apply(const uint32_t* pairs, int64_t count, int64_t v_begin,
+                                                      int64_t v_end, const uint32_t* hoff, const int32_t* hadj,
+                                                      uint8_t* fmp, int64_t plane, uint32_t np) {
+  const int64_t T = (int64_t)gridDim.x * BLOCK;
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < count; i += T) {
+    const uint32_t w = pairs[2 * i], word = pairs[2 * i + 1];
+    if (!(word & SW<uint32_t>::COMMIT) || ((int64_t)w >= v_begin && (int64_t)w < v_end)) continue;
+    const uint32_t c = word & SW<uint32_t>::CMASK;
+    if (c == 0 || c > 8u * np) continue;
+    uint8_t* pl = fmp + (int64_t)((c - 1) >> 3) * plane;
+    const uint32_t bit = 1u << ((c - 1) & 7);
+    for (uint32_t j = hoff[w]; j < hoff[w + 1]; ++j) red_plane<uint32_t>(pl, hadj[j], bit);
+  }
+}
+
 }  // namespace gcdev
 
 struct gc_dist {
@@ -76,7 +127,10 @@ struct gc_dist {
   uint32_t* d_off = nullptr;         // device copies for k_pack
   uint32_t* d_cnt = nullptr;
   unsigned long long* d_count = nullptr;
-  void* mem[8] = {};
+  void* mem[16] = {};
+  uint8_t* boundary = nullptr;       // local vertices with a remote neighbour (the only ones packed)
+  uint32_t* hoff = nullptr;          // halo adjacency (push First-Fit across partitions)
+  int32_t* hadj = nullptr;
   int nmem = 0;
 };
 
@@ -94,8 +148,8 @@ gc_status dist_fail(gc_dist* h, cudaError_t e, const char* what) {
   } while (0)
 
 void launch_dist_b(gc_dist* h, int grid, const Params& p, uint32_t r, WE* W, WE* Wo) {
-  if (h->policy == HIGHER_ID) k_phase_b<HIGHER_ID, false, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
-  else k_phase_b<LOWER_ID, false, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
+  if (h->policy == HIGHER_ID) k_phase_b<HIGHER_ID, true, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
+  else k_phase_b<LOWER_ID, true, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
 }
 
 }  // namespace
@@ -156,8 +210,12 @@ gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64
   h->v_begin = v_begin;
   h->v_end = v_end;
   h->max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)(n_global + 1 > 0xffffffffLL ? 0xffffffffu : n_global + 1);
+  // workspace from the per-device stream-ordered pool (cached across partitions: creating
+  // and destroying a partition per colouring costs no cudaMalloc/cudaFree)
+  cudaMemPool_t pool;
+  if ((e = get_pool(h->dev, &pool)) != cudaSuccess) { gc_dist_destroy(h); return cuda_fail(e, "get_pool"); }
   auto alloc = [&](void** q, size_t bytes) {
-    cudaError_t ee = cudaMalloc(q, bytes ? bytes : 16);
+    cudaError_t ee = cudaMallocFromPoolAsync(q, bytes ? bytes : 16, pool, h->stream);
     if (ee == cudaSuccess) h->mem[h->nmem++] = *q;
     return ee;
   };
@@ -170,8 +228,26 @@ gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64
     gc_dist_destroy(h);
     return cuda_fail(e, "gc_dist_create: cudaMalloc");
   }
+  // forbidden-colour planes indexed by global id (only the local bytes are ever read)
+  const int64_t pitch = (n_global + 255) / 256 * 256;
+  uint32_t np = (uint32_t)MAX_PLANES;
+  if ((uint64_t)np * (uint64_t)pitch > (16ull << 30)) {
+    const uint64_t fit = (16ull << 30) / (uint64_t)pitch;
+    np = fit < 16 ? 16u : (uint32_t)fit;
+  }
+  void *planes, *hoff, *hcur, *bnd;
+  if ((e = alloc(&planes, (size_t)pitch * np)) != cudaSuccess ||
+      (e = alloc(&bnd, (size_t)(nl ? nl : 1))) != cudaSuccess ||
+      (e = alloc(&hoff, sizeof(uint32_t) * (size_t)(n_global + 1))) != cudaSuccess ||
+      (e = alloc(&hcur, sizeof(uint32_t) * (size_t)(n_global + 1))) != cudaSuccess) {
+    gc_dist_destroy(h);
+    return cuda_fail(e, "gc_dist_create: cudaMalloc");
+  }
   memset(&h->p, 0, sizeof(h->p));
   Params& p = h->p;
+  p.fmp = (uint8_t*)planes;
+  p.plane = pitch;
+  p.np = np;
   p.n = (int32_t)nl;
   p.v_base = (int32_t)v_begin;
   p.rp = row_ptr_local;
@@ -194,9 +270,36 @@ gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64
   k_fill_u32<<<h->grid, BLOCK, 0, s>>>((uint32_t*)st, n_global, 1u);
   DK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
   if (nl > 0) {
-    k_prologue_count<false><<<h->grid, BLOCK, 0, s>>>(p);
+    k_prologue_count<true><<<h->grid, BLOCK, 0, s>>>(p);
     k_prologue_scatter<<<h->grid, BLOCK, 0, s>>>(p);
   }
+  // halo adjacency: counts per remote vertex -> offsets -> lists
+  DK(cudaMemsetAsync(hoff, 0, sizeof(uint32_t) * (size_t)(n_global + 1), s));
+  if (nl > 0) k_halo_count<<<h->grid, BLOCK, 0, s>>>(p, nl, v_begin, v_end, (uint32_t*)hoff, (uint8_t*)bnd);
+  h->boundary = (uint8_t*)bnd;
+  {  // exclusive scan (CUB) of the n_global + 1 counters into hcur, then back to hoff
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (uint32_t*)hoff, (uint32_t*)hcur, (int)(n_global + 1), s);
+    void* tmp;
+    if ((e = alloc(&tmp, tmp_bytes)) != cudaSuccess) {
+      gc_dist_destroy(h);
+      return cuda_fail(e, "gc_dist_create: cudaMalloc");
+    }
+    DK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, (uint32_t*)hoff, (uint32_t*)hcur, (int)(n_global + 1), s));
+    DK(cudaMemcpyAsync(hoff, hcur, sizeof(uint32_t) * (size_t)(n_global + 1), cudaMemcpyDeviceToDevice, s));
+  }
+  uint32_t nhalo = 0;
+  DK(cudaMemcpyAsync(&nhalo, (uint32_t*)hoff + n_global, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  DK(cudaStreamSynchronize(s));
+  void* hadj;
+  if ((e = alloc(&hadj, sizeof(int32_t) * (size_t)(nhalo ? nhalo : 1))) != cudaSuccess) {
+    gc_dist_destroy(h);
+    return cuda_fail(e, "gc_dist_create: cudaMalloc");
+  }
+  DK(cudaMemcpyAsync(hcur, hoff, sizeof(uint32_t) * (size_t)(n_global + 1), cudaMemcpyDeviceToDevice, s));
+  if (nl > 0) k_halo_fill<<<h->grid, BLOCK, 0, s>>>(p, nl, v_begin, v_end, (uint32_t*)hcur, (int32_t*)hadj);
+  h->hoff = (uint32_t*)hoff;
+  h->hadj = (int32_t*)hadj;
   DK(cudaGetLastError());
   DevInfo hi;
   DK(cudaMemcpyAsync(&hi, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
@@ -217,7 +320,7 @@ gc_status gc_dist_phase_a(gc_dist* h) {
   g_err[0] = 0;
   if (!h) return GC_ERR_INVALID_ARGUMENT;
   if (h->round > 1 && h->p.n > 0) {
-    k_phase_a<false, false><<<h->grid, BLOCK, 0, h->stream>>>(h->p, h->round, h->W[h->cur]);
+    k_phase_a<true, false><<<h->grid, BLOCK, 0, h->stream>>>(h->p, h->round, h->W[h->cur]);
     DK(cudaGetLastError());
   }
   DK(cudaStreamSynchronize(h->stream));
@@ -255,7 +358,7 @@ gc_status gc_dist_pack(gc_dist* h, int32_t what, uint32_t* pairs, uint64_t* coun
   DK(cudaMemcpyAsync(h->d_cnt, h->cnt_in, sizeof(h->cnt_in), cudaMemcpyHostToDevice, h->stream));
   DK(cudaMemsetAsync(h->d_count, 0, sizeof(unsigned long long), h->stream));
   k_pack<<<h->grid, BLOCK, 0, h->stream>>>(h->W[h->cur], h->d_off, h->d_cnt, (const uint32_t*)h->p.st, what, pairs,
-                                           h->d_count);
+                                           h->d_count, h->boundary, h->p.v_base);
   DK(cudaGetLastError());
   unsigned long long c = 0;
   DK(cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
@@ -269,6 +372,9 @@ gc_status gc_dist_unpack(gc_dist* h, const uint32_t* pairs, uint64_t count) {
   if (!h || (count && !pairs)) return GC_ERR_INVALID_ARGUMENT;
   if (count) {
     k_unpack<<<h->grid, BLOCK, 0, h->stream>>>(pairs, (int64_t)count, (uint32_t*)h->p.st);
+    if (h->p.n > 0)
+      k_halo_apply<<<h->grid, BLOCK, 0, h->stream>>>(pairs, (int64_t)count, h->v_begin, h->v_end, h->hoff, h->hadj,
+                                                     h->p.fmp, h->p.plane, h->p.np);
     DK(cudaGetLastError());
   }
   DK(cudaStreamSynchronize(h->stream));
@@ -311,8 +417,11 @@ gc_status gc_dist_finalize(gc_dist* h, uint32_t* colors_local, uint32_t* max_col
 
 gc_status gc_dist_destroy(gc_dist* h) {
   if (!h) return GC_OK;
-  for (int i = 0; i < h->nmem; ++i) cudaFree(h->mem[i]);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  for (int i = 0; i < h->nmem; ++i) cudaFreeAsync(h->mem[i], h->stream);
+  if (h->stream) {
+    cudaStreamSynchronize(h->stream);
+    cudaStreamDestroy(h->stream);
+  }
   delete h;
   return GC_OK;
 }

@@ -39,7 +39,7 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       maxdeg = max(maxdeg, (uint32_t)min(deg, (int64_t)0xffffffff));
       b = bin_of(p, deg);
       sts(st + p.v_base + v, 1u);
-      if (PUSH) sts(p.fmp + v, 0u);
+      if (PUSH) sts(p.fmp + p.v_base + v, 0u);  // planes are indexed by global id
       if (p.dirty) sts(p.dirty + v, 0u);
       e.k = 0;
       if (dense && POL != DEGREE) {
