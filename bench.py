@@ -243,9 +243,10 @@ def run_partitioned(args, g, rank, world, local):
             "num_colors": res.num_colors, "rounds": res.rounds,
             "exchanged_pairs_rank0": res.exchanged_pairs,
             "timing": "host wall clock between barriers (every dist call is synchronous), max over ranks",
-            # per step: 3 ingest kernels, per round phase A + pack + unpack (r > 1) and
-            # phase B + pack + unpack, 1 finalize
-            "gpu_launches": args.steps * (3 + 6 * res.rounds - 3 + 1), "clocks": clk,
+            # per step: create (fill, 2 ingest, halo count, CUB scan (2), halo fill = 7); round 1:
+            # phase B + pack + unpack + halo apply; rounds >= 2: 8 (phase A, pack, unpack, halo
+            # apply, phase B, pack, unpack, halo apply); finalize 1
+            "gpu_launches": args.steps * (7 + 4 + 8 * (res.rounds - 1) + 1), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     return 0

@@ -480,7 +480,8 @@ template <int POL>
 __device__ __forceinline__ bool recolors(const Params& p, int32_t v, int32_t w, int64_t dv) {
   if (POL == HIGHER_ID) return v > w;
   if (POL == LOWER_ID) return v < w;
-  const int64_t dw = RP(p, w + 1) - RP(p, w);  // one partition only (DEGREE is single-GPU)
+  // one partition only (DEGREE is single-GPU); dense runs keep the degrees in ksplit
+  const int64_t dw = p.ksplit ? (int64_t)ldks(p.ksplit + w) : RP(p, w + 1) - RP(p, w);
   return dv < dw || (dv == dw && v > w);
 }
 

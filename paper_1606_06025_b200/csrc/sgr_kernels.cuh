@@ -45,6 +45,8 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       if (dense && POL != DEGREE) {
         e.k = b == 0 ? split_fast(p, e.v, e.beg, end) : row_split(p, e.v, e.beg, end);
         p.ksplit[v] = e.k;
+      } else if (dense) {
+        p.ksplit[v] = (int32_t)deg;  // DEGREE: the array holds the degrees (one load per compare)
       }
     }
 #pragma unroll
