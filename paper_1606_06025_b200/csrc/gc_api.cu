@@ -437,6 +437,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
   p.dense_div = dense_div;
   if (const char* c = getenv("GC_COMPACT")) p.compact = (uint32_t)atoi(c);
+  if (const char* c = getenv("GC_N1_CHG")) p.n1chg = (uint32_t)atoi(c);
   p.dense_div_n1 = 16;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16
   if (const char* dd = getenv("GC_DENSE_DIV_N1")) p.dense_div_n1 = (uint32_t)atoi(dd);
   if (const char* dd = getenv("GC_DENSE_DIV")) p.dense_div_n1 = (uint32_t)atoi(dd);  // one knob for tests

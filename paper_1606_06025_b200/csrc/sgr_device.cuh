@@ -129,6 +129,7 @@ struct Params {
   uint32_t n1;                  // dirty-set rounds enabled
   uint32_t davg2;               // average successors + 1 (m/2n + 1, rounded up): N1 cost model
   uint32_t n1gain;              // min(m/2n, 8): N1 saving per clean vertex, in units of marks
+  uint32_t n1chg;               // 0: mark every round; else only when chg(r-1) * n1chg < |W_r|
   WE* heavy;                    // dense mode: the vertices of degree > t3 {v, split, row start}
   WE* wl0;                      // worklist buffers, n entries each, bin segments
   WE* wl1;

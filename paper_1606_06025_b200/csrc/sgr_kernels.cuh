@@ -1457,7 +1457,9 @@ __global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_persistent(Params p) {
     // round marks on the 27-point stencil (-22 %) and the mesh (-4 %); on R-MAT marking the
     // hub rows costs more than it saves (2.4x slower when forced), and a per-round cost model
     // based on the previous round's tentative-colour changes did no better than this rule
-    const bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && ld_relaxed(&p.info->maxdeg) <= 64u));
+    bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && ld_relaxed(&p.info->maxdeg) <= 64u));
+    if (mark && p.n1 == 1 && p.n1chg)  // optional: only once the previous round changed few colours
+      mark = r >= 3 && (uint64_t)ld_relaxed(&p.info->chg[(r - 1) % 3]) * p.n1chg < tot;
     if (r > 1) {
       if (list) phase_a_list<S, POL, CW>(p, r, wk);
       else if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);

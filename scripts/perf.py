@@ -45,6 +45,8 @@ def main():
     variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
     variants["compact"] = [dict(), dict(env={"GC_COMPACT": "1"}), dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "16"}),
                            dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "64"})]
+    variants["n1chg"] = [dict(), dict(env={"GC_N1": "0", "GC_DENSE_DIV": "16"}), dict(env={"GC_N1_CHG": "2"}),
+                         dict(env={"GC_N1_CHG": "4"}), dict(env={"GC_N1_CHG": "8"}), dict(env={"GC_N1_CHG": "16"})]
     variants["list"] = [dict(env={"GC_LIST": x}) for x in ("0", "1", "2")]
     variants["n1"] = [dict(env={"GC_N1": x}) for x in ("0", "1", "2")]
     variants["dense"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("0", "2", "4", "8", "16", "64")]
