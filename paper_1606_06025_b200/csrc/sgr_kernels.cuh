@@ -25,15 +25,24 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   bool wide = false;
   uint32_t maxdeg = 0;
+  // the row offsets of the next iteration's vertex are loaded one iteration ahead, so that
+  // their latency overlaps this vertex's split search
+  const int64_t first = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31) + lane;
+  int64_t nbeg = first < p.n ? ldr(p.rp, first) : 0, nend = first < p.n ? ldr(p.rp, first + 1) : 0;
   for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
     int b = -1;
     WE e;
+    const int64_t cbeg = nbeg, cend_ = nend;
+    if (v + stride < p.n) {
+      nbeg = ldr(p.rp, v + stride);
+      nend = ldr(p.rp, v + stride + 1);
+    }
     if (act) {
       e.v = (int32_t)(p.v_base + v);
-      e.beg = ldr(p.rp, v);
-      const int64_t end = ldr(p.rp, v + 1);
+      e.beg = cbeg;
+      const int64_t end = cend_;
       const int64_t deg = end - e.beg;
       if (sizeof(S) < 4 && deg > NARROW_MAX_DEG) wide = true;
       maxdeg = max(maxdeg, (uint32_t)min(deg, (int64_t)0xffffffff));
