@@ -101,8 +101,8 @@ typedef struct gc_opts {
   uint32_t flags;            /* GC_FLAG_*; default GC_FLAG_VALIDATE */
   uint32_t max_rounds;       /* 0 -> n + 1 (reading C13) */
   int32_t device;            /* CUDA ordinal; -1 = the calling thread's current device */
-  uint32_t thread_bin_max;   /* a winner of degree <= this scatters its colour bit by itself,
-                                larger ones with the whole warp (0 -> default 16) */
+  uint32_t thread_bin_max;   /* reserved: ignored since the commit scatters are warp-flattened
+                                (kept for ABI stability) */
   uint32_t warp_bin_max;     /* degree <= this -> thread probe + warp continuation per vertex
                                 (0 -> default 512); larger degrees -> one CTA per vertex
                                 (load balancing) */
