@@ -152,8 +152,16 @@ void* pick_persistent_s(int pol, bool push, bool cw) {
   return nullptr;
 }
 
-// state-word width: 1, 2 or 4 bytes
-void* pick_persistent(int sbytes, int pol, bool push, bool cw) {
+template <int POL, bool CW>
+void* fat_ptr() { return (void*)sgr_persistent_fat<POL, CW>; }
+
+// state-word width: 1, 2 or 4 bytes; fat: the 3-CTA/SM variant (8-bit words, push mode)
+void* pick_persistent(int sbytes, int pol, bool push, bool cw, bool fat = false) {
+  if (fat && sbytes == 1 && push) {
+    if (pol == HIGHER_ID) return cw ? fat_ptr<HIGHER_ID, true>() : fat_ptr<HIGHER_ID, false>();
+    if (pol == LOWER_ID) return cw ? fat_ptr<LOWER_ID, true>() : fat_ptr<LOWER_ID, false>();
+    return cw ? fat_ptr<DEGREE, true>() : fat_ptr<DEGREE, false>();
+  }
   if (sbytes == 1) return pick_persistent_s<uint8_t>(pol, push, cw);
   if (sbytes == 2) return pick_persistent_s<uint16_t>(pol, push, cw);
   return pick_persistent_s<uint32_t>(pol, push, cw);
@@ -524,6 +532,20 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     // 8-bit state words first; a colour > 127 makes the kernel stop at the next barrier with
     // ST_NEED16 and a vertex of degree > 32766 stops it in its prologue with ST_NEED32; the
     // run is then repeated with the wider words (at most two restarts).
+    // kernel variant: bounded degree (<= 64) and >= 8 entries per row -> 3 CTAs/SM (sgr_kernels.cuh)
+    bool fat = false;
+    if (push && n1 && m >= 8 * n) {
+      void* dmax;
+      CK(sc.alloc(&dmax, sizeof(uint32_t)));
+      CK(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
+      k_maxdeg<<<prop.sms * 8, BLOCK, 0, s>>>((int32_t)n, d_rp, (uint32_t*)dmax);
+      CK(cudaGetLastError());
+      uint32_t mx = 0;
+      CK(cudaMemcpyAsync(&mx, dmax, sizeof(mx), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      fat = mx <= 64;
+    }
+    if (const char* f = getenv("GC_FAT")) fat = f[0] == '1';
     sbytes = 1;
     if (const char* sw = getenv("GC_STATE_BYTES")) {  // diagnostics: force a width
       const int f = atoi(sw);
@@ -532,7 +554,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     for (int attempt = 0; attempt < 3; ++attempt) {
       p.st = (uint8_t*)planes - (int64_t)sbytes * pitch;
       CK(set_window(sbytes));
-      void* fn = pick_persistent(sbytes, (int)o.policy, push, cw);
+      void* fn = pick_persistent(sbytes, (int)o.policy, push, cw, fat);
       int per_sm = 0;
       CK(occupancy(dev, fn, &per_sm));
       if (per_sm < 1) {

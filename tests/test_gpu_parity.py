@@ -92,7 +92,8 @@ def test_parity_variants(gc, kw):
                                  dict(GC_N1="2", GC_DENSE_DIV="1"), dict(GC_N1="2", GC_DENSE_DIV="1000000000"),
                                  dict(GC_N1="2", GC_STATE_BYTES="2"), dict(GC_LIST="0"), dict(GC_LIST="2"),
                                  dict(GC_LIST="2", GC_N1="2"), dict(GC_LIST="2", GC_DENSE_DIV="1"),
-                                 dict(GC_COMPACT="1"), dict(GC_COMPACT="1", GC_N1="0")],
+                                 dict(GC_COMPACT="1"), dict(GC_COMPACT="1", GC_N1="0"), dict(GC_FAT="1"),
+                                 dict(GC_FAT="1", GC_N1="2", GC_DENSE_DIV="1"), dict(GC_FAT="0")],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_parity_env_variants(gc, env, monkeypatch):
     """Forced state-word widths, filtered commit scatter, no L2 window: same result."""
