@@ -136,6 +136,11 @@ void gc_opts_default(gc_opts* o);
  *   num_colors max colour (= number of distinct colours, First-Fit fixpoint).
  *   rounds     number of SGR rounds (Phase-A passes; PAPER.md:427 loop iterations).
  * n = 0 returns GC_OK with num_colors = rounds = 0.
+ * Workspace (device, from a per-device stream-ordered pool, freed before return): about
+ * 110 bytes per vertex (state words + up to 64 forbidden-colour byte planes, of which only the
+ * planes a run reaches are touched; splits; dirty marks; two 16-byte worklists) plus 16 bytes
+ * per vertex of degree > 512.  The colouring runs as one cooperative kernel occupying every SM;
+ * concurrent calls on other streams wait for it (they never interleave).
  */
 gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                    const gc_opts* opts, uint32_t* colors_out, uint32_t* num_colors,
