@@ -360,7 +360,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   CK(sc.alloc(&hot, (size_t)pitch * (4 + np)));
   planes = (uint8_t*)hot + 4 * pitch;
   // dense rounds (push mode, persistent driver): per-vertex split + static heavy-vertex list
-  uint32_t dense_div = 4;  // sweep (R-MAT s24, stencil 128^3, mesh 8192^2): 2..64 -> 4
+  uint32_t dense_div = 3;  // sweep on R-MAT s24 (2, 3, 4, 6 -> 3; dirty-set graphs use dense_div_n1)
   if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
   if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
   const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 512;
