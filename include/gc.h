@@ -104,7 +104,7 @@ typedef struct gc_opts {
   uint32_t thread_bin_max;   /* reserved: ignored since the commit scatters are warp-flattened
                                 (kept for ABI stability) */
   uint32_t warp_bin_max;     /* degree <= this -> thread probe + warp continuation per vertex
-                                (0 -> default 512); larger degrees -> one CTA per vertex
+                                (0 -> default 1024); larger degrees -> one CTA per vertex
                                 (load balancing) */
   uint32_t blocks_per_sm;    /* persistent grid = SMs x this (0 -> max co-resident) */
   void* stream;              /* cudaStream_t to run on; NULL = library-internal stream */
@@ -139,7 +139,7 @@ void gc_opts_default(gc_opts* o);
  * Workspace (device, from a per-device stream-ordered pool, freed before return): about
  * 110 bytes per vertex (state words + up to 64 forbidden-colour byte planes, of which only the
  * planes a run reaches are touched; splits; dirty marks; two 16-byte worklists) plus 16 bytes
- * per vertex of degree > 512.  The colouring runs as one cooperative kernel occupying every SM;
+ * per vertex of degree > 1024.  The colouring runs as one cooperative kernel occupying every SM;
  * concurrent calls on other streams wait for it (they never interleave).
  */
 gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,

@@ -258,7 +258,7 @@ gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64
   p.info = (DevInfo*)info;
   p.max_rounds = h->max_rounds;
   p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
-  p.t3 = o.warp_bin_max ? o.warp_bin_max : 512;
+  p.t3 = o.warp_bin_max ? o.warp_bin_max : 1024;
   p.timeout_ns = 60ull * 1000000000ull;
   h->W[0] = (WE*)w0;
   h->W[1] = (WE*)w1;

@@ -363,7 +363,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   uint32_t dense_div = 3;  // sweep on R-MAT s24 (2, 3, 4, 6 -> 3; dirty-set graphs use dense_div_n1)
   if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
   if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
-  const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 512;
+  const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 1024;
   void *ksplit = nullptr, *heavy = nullptr, *dirty = nullptr, *wlw0 = nullptr, *wlw1 = nullptr, *dlist = nullptr;
   uint32_t list_ok = 0;  // list rounds (GC_LIST: 0 off (default: slower on every config
                          // measured), 1 cost rule, 2 from round 3 on)
@@ -442,7 +442,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.colors_out = (uint32_t*)dcol;
   p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n + 1 > 0xffffffffu ? 0xffffffffu : n + 1);
   p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
-  p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/1024/4096 -> 512 best
+  p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/768/1024/1536/2048 -> 1024 best
   p.dense_div = dense_div;
   if (const char* c = getenv("GC_COMPACT")) p.compact = (uint32_t)atoi(c);
   if (const char* c = getenv("GC_N1_CHG")) p.n1chg = (uint32_t)atoi(c);
