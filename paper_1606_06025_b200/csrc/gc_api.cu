@@ -445,6 +445,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/768/1024/1536/2048 -> 1024 best
   p.dense_div = dense_div;
   if (const char* c = getenv("GC_COMPACT")) p.compact = (uint32_t)atoi(c);
+  p.dch = 16;  // sweep 2..32 on the three configs: 16 (R-MAT s24 -1 %)
+  if (const char* c = getenv("GC_DCH")) p.dch = (uint32_t)atoi(c) ? (uint32_t)atoi(c) : 16u;
   if (const char* c = getenv("GC_N1_CHG")) p.n1chg = (uint32_t)atoi(c);
   p.dense_div_n1 = 16;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16
   if (const char* dd = getenv("GC_DENSE_DIV_N1")) p.dense_div_n1 = (uint32_t)atoi(dd);

@@ -120,6 +120,7 @@ struct Params {
   uint32_t dense_div;           // dense rounds while |W_r| * dense_div > n (0: always sparse)
   uint32_t dense_div_n1;        // the same in dirty-set rounds
   uint32_t compact;             // dense Phase B lists the pending vertices (also without marks)
+  uint32_t dch;                 // dense sweeps: about n / (dch x warps) vertices per queue pop
   int32_t* ksplit;              // dense mode: number of lower-id neighbours of every vertex
   uint8_t* dirty;               // dirty-set rounds (N1): Phase B re-examines only marked vertices
   int32_t* wlw0;                // list rounds: winners of even / odd rounds (capacity n each)

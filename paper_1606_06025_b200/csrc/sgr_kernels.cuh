@@ -1379,7 +1379,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
     return;
   }
-  const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (8u * nwarps)) / WB * WB));
+  const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (p.dch * nwarps)) / WB * WB));
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nv; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
     for (uint32_t bse = c0; bse < cend; bse += WB)

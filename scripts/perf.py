@@ -51,6 +51,7 @@ def main():
     variants["n1"] = [dict(env={"GC_N1": x}) for x in ("0", "1", "2")]
     variants["dense"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("0", "2", "4", "8", "16", "64")]
     variants["t3"] = [dict(warp_bin_max=t) for t in (512, 768, 1024, 1536, 2048)]
+    variants["dch"] = [dict(env={"GC_DCH": d}) for d in ("2", "4", "8", "16", "32")]
     variants["div"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("2", "3", "4", "6")]
     variants["densen1"] = [dict(env={"GC_DENSE_DIV": d, "GC_N1": "2"}) for d in ("4", "8", "16", "32", "64", "256")]
     variants["env"] = [dict(), dict(env={"GC_SCATTER_FILTER": "1"}), dict(env={"GC_STATE_BYTES": "2"}),
