@@ -125,7 +125,10 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
 #ifndef GC_FLAT_U
 #define GC_FLAT_U 2
 #endif
-constexpr int FLAT_U = GC_FLAT_U;  // items per lane per step (independent loads in flight)
+constexpr int FLAT_U = GC_FLAT_U;
+#ifndef GC_CAPMUL
+#define GC_CAPMUL 4           // growth of the conflict-scan pass length after the first two passes
+#endif  // items per lane per step (independent loads in flight)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 #pragma unroll
@@ -641,7 +644,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         }
       }
     }
-    cap = cap < 1024 ? (cap == (uint32_t)PROBE ? 3 * PROBE : cap * 4) : cap;  // 4, 12, 48, 192, 768, ...
+    cap = cap < 1024 ? (cap == (uint32_t)PROBE ? 3 * PROBE : cap * GC_CAPMUL) : cap;  // 4, 12, 48, 192, 768, ...
   }
   // winners commit; the forbidden masks of their neighbours get their colour bit
   const bool win = state == 2;
@@ -1012,7 +1015,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       }
     }
     __syncwarp();
-    cap = cap < 1024 ? cap * 4 : cap;  // 12, 48, 192, 768, ...
+    cap = cap < 1024 ? cap * GC_CAPMUL : cap;  // 12, 48, 192, 768, ...
   }
   // commit: winners set the top bit of their own state word
 #pragma unroll
