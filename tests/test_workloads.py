@@ -61,3 +61,50 @@ def test_mesh_deletion_fraction():
 def test_splitmix64_reference_value():
     # first output of SplitMix64 seeded with 0 (Vigna's reference: x += golden gamma, mix)
     assert wl.splitmix64(0) == 0xE220A8397B1DCDAF
+
+
+def _rmat_python(scale, ef, abc, seed):
+    """Plain-Python transcription of the W1 recipe for tiny scales."""
+    M = (1 << 64) - 1
+
+    def sm(x):
+        z = (x + 0x9E3779B97F4A7C15) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    a, b, c = abc
+    n = 1 << scale
+    pi = list(range(n))
+    for i in range(n - 1, 0, -1):
+        j = sm((seed ^ 0x5851F42D4C957F2D) + (n - 1 - i)) % (i + 1)
+        pi[i], pi[j] = pi[j], pi[i]
+    adj = [set() for _ in range(n)]
+    for i in range(ef * n):
+        u = v = 0
+        for l in range(scale):
+            r = (sm(((seed << 40) + 64 * i + l) & M) >> 11) * 2.0 ** -53
+            bu, bv = (0, 0) if r < a else (0, 1) if r < a + b else (1, 0) if r < a + b + c else (1, 1)
+            u, v = (u << 1) | bu, (v << 1) | bv
+        pu, pv = pi[u], pi[v]
+        if pu != pv:
+            adj[pu].add(pv)
+            adj[pv].add(pu)
+    return adj
+
+
+@pytest.mark.parametrize("abc,seed", [(wl.RMAT_G, 1), (wl.GRAPH500, 7)])
+def test_rmat_matches_python_recipe(abc, seed):
+    g = wl.rmat(7, 8, abc, seed)
+    adj = _rmat_python(7, 8, abc, seed)
+    for v in range(g.n):
+        assert g.adj(v).tolist() == sorted(adj[v])
+
+
+@pytest.mark.parametrize("bounds", [[0, 1000, 2500, 4096], [0, 0, 17, 4095, 4096], [0, 4096]])
+def test_rmat_range_equals_whole_graph(bounds):
+    """Rows generated per vertex range (multi-GPU ranks, scale 27) equal the whole graph's."""
+    g = wl.rmat(12, 16)
+    for b, e in zip(bounds[:-1], bounds[1:]):
+        rp, ci = wl.rmat_range(12, 16, b, e)
+        assert np.array_equal(rp, g.row_ptr[b:e + 1] - g.row_ptr[b])
+        assert np.array_equal(ci, g.col_idx[g.row_ptr[b]:g.row_ptr[e]])

@@ -41,6 +41,9 @@ def _load():
         i64pp = ctypes.POINTER(ctypes.POINTER(ctypes.c_int64))
         lib.gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_uint64, i64p, i64p, i64pp, i32pp]
+        lib.gen_rmat_range.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                       i64p, i64pp, i32pp]
         lib.gen_stencil27.argtypes = [ctypes.c_int32] * 3 + [i64p, i64p, i64pp, i32pp]
         lib.gen_mesh2d.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
                                    i64p, i64p, i64pp, i32pp]
@@ -49,7 +52,7 @@ def _load():
         lib.gen_splitmix64.argtypes = [ctypes.c_uint64]
         lib.gen_splitmix64.restype = ctypes.c_uint64
         lib.gen_free.argtypes = [ctypes.c_void_p]
-        for f in ("gen_rmat", "gen_stencil27", "gen_mesh2d", "gen_from_edges"):
+        for f in ("gen_rmat", "gen_rmat_range", "gen_stencil27", "gen_mesh2d", "gen_from_edges"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -113,6 +116,21 @@ def rmat(scale: int, edge_factor: int, abc=RMAT_G, seed: int = 1) -> Graph:
     a, b, c = abc
     n, rp, ci = _call(_load().gen_rmat, scale, edge_factor, a, b, c, seed)
     return Graph(n, rp, ci, f"rmat_s{scale}_ef{edge_factor}")
+
+
+def rmat_range(scale: int, edge_factor: int, v_begin: int, v_end: int, abc=RMAT_G, seed: int = 1):
+    """Rows [v_begin, v_end) of rmat(scale, edge_factor, abc, seed) without building the whole
+    graph: (row_ptr int64[v_end-v_begin+1] rebased to 0, col_idx int32 in GLOBAL ids).  Used by
+    the multi-GPU bench (each rank generates only its own vertex range) and for scale 27."""
+    a, b, c = abc
+    m = ctypes.c_int64()
+    rp = ctypes.POINTER(ctypes.c_int64)()
+    ci = ctypes.POINTER(ctypes.c_int32)()
+    rc = _load().gen_rmat_range(scale, edge_factor, a, b, c, seed, v_begin, v_end, ctypes.byref(m),
+                                ctypes.byref(rp), ctypes.byref(ci))
+    if rc != 0:
+        raise ValueError(f"gen_rmat_range failed with code {rc}")
+    return _adopt(rp, v_end - v_begin + 1, np.int64), _adopt(ci, m.value, np.int32)
 
 
 def stencil27(nx: int, ny: int | None = None, nz: int | None = None) -> Graph:

@@ -149,55 +149,120 @@ static int csr_from_arcs(int64_t n, const int32_t* src, const int32_t* dst, int6
  *   r = (splitmix64(seed*2^40 + 64*i + l) >> 11) * 2^-53 and picks the quadrant from the
  *   cumulative (a, a+b, a+b+c); u,v built MSB first; both ends relabelled by the seeded
  *   Fisher-Yates permutation pi; both directions added, self loops dropped, deduped.
+ *
+ * gen_rmat_range builds only the rows [vb, ve) (column ids global), without ever holding the
+ * arc list: every sample is recomputed from its counter in two passes (degree count, then
+ * scatter), so the memory is the rows' own CSR plus n int32 for pi.  The rows are identical
+ * to the same rows of the whole graph (each row is the sorted, deduplicated set of its
+ * neighbours), so ranges can be generated independently per rank (BASELINE configs[4],
+ * scale 27: 4.3e9 entries).
  */
-int gen_rmat(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
-             int64_t* n_out, int64_t* m_out, int64_t** row_ptr_out, int32_t** col_out) {
+static inline void rmat_sample(int32_t scale, uint64_t base, int64_t i, double a, double ab, double abc,
+                               uint64_t* u_out, uint64_t* v_out) {
+  uint64_t u = 0, v = 0;
+  for (int l = 0; l < scale; ++l) {
+    double r = (double)(splitmix64(base + 64ULL * (uint64_t)i + (uint64_t)l) >> 11) * 0x1.0p-53;
+    uint64_t bu, bv;
+    if (r < a) { bu = 0; bv = 0; }
+    else if (r < ab) { bu = 0; bv = 1; }
+    else if (r < abc) { bu = 1; bv = 0; }
+    else { bu = 1; bv = 1; }
+    u = (u << 1) | bu;
+    v = (v << 1) | bv;
+  }
+  *u_out = u;
+  *v_out = v;
+}
+
+int gen_rmat_range(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                   int64_t vb, int64_t ve, int64_t* m_out, int64_t** row_ptr_out, int32_t** col_out) {
   if (scale < 1 || scale > 30 || edge_factor < 0) return 1;
-  int64_t n = (int64_t)1 << scale;
-  int64_t ns = edge_factor * n;
+  const int64_t n = (int64_t)1 << scale;
+  if (vb < 0 || ve < vb || ve > n) return 1;
+  const int64_t nl = ve - vb;
+  const int64_t ns = edge_factor * n;
   int32_t* pi = (int32_t*)malloc((size_t)n * sizeof(int32_t));
-  if (!pi) return 2;
+  int64_t* off = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
+  int64_t* cur = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
+  if (!pi || !off || !cur) { free(pi); free(off); free(cur); return 2; }
   for (int64_t i = 0; i < n; ++i) pi[i] = (int32_t)i;
   for (int64_t i = n - 1; i >= 1; --i) {
     uint64_t j = splitmix64((seed ^ 0x5851F42D4C957F2DULL) + (uint64_t)(n - 1 - i)) % (uint64_t)(i + 1);
     int32_t t = pi[i]; pi[i] = pi[j]; pi[j] = t;
   }
-  int32_t* src = (int32_t*)malloc((size_t)(2 * ns > 0 ? 2 * ns : 1) * sizeof(int32_t));
-  int32_t* dst = (int32_t*)malloc((size_t)(2 * ns > 0 ? 2 * ns : 1) * sizeof(int32_t));
-  uint8_t* keep = (uint8_t*)malloc((size_t)(ns > 0 ? ns : 1));
-  if (!src || !dst || !keep) { free(pi); free(src); free(dst); free(keep); return 2; }
   const double ab = a + b, abc = a + b + c;
   const uint64_t base = seed << 40;
+  /* pass 1: arcs per local row (both directions of every non-loop sample, duplicates kept) */
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < ns; ++i) {
-    uint64_t u = 0, v = 0;
-    for (int l = 0; l < scale; ++l) {
-      double r = (double)(splitmix64(base + 64ULL * (uint64_t)i + (uint64_t)l) >> 11) * 0x1.0p-53;
-      uint64_t bu, bv;
-      if (r < a) { bu = 0; bv = 0; }
-      else if (r < ab) { bu = 0; bv = 1; }
-      else if (r < abc) { bu = 1; bv = 0; }
-      else { bu = 1; bv = 1; }
-      u = (u << 1) | bu;
-      v = (v << 1) | bv;
+    uint64_t u, v;
+    rmat_sample(scale, base, i, a, ab, abc, &u, &v);
+    const int64_t pu = pi[u], pv = pi[v];
+    if (pu == pv) continue;
+    if (pu >= vb && pu < ve) {
+#pragma omp atomic
+      cur[pu - vb]++;
     }
-    int32_t pu = pi[u], pv = pi[v];
-    keep[i] = (uint8_t)(pu != pv);
-    src[2 * i] = pu; dst[2 * i] = pv;
-    src[2 * i + 1] = pv; dst[2 * i + 1] = pu;
+    if (pv >= vb && pv < ve) {
+#pragma omp atomic
+      cur[pv - vb]++;
+    }
+  }
+  prefix_sum(cur, off, nl);
+  const int64_t k = off[nl];
+  int32_t* col = (int32_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int32_t));
+  if (!col) { free(pi); free(off); free(cur); return 2; }
+  memcpy(cur, off, (size_t)nl * sizeof(int64_t));
+  /* pass 2: scatter */
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < ns; ++i) {
+    uint64_t u, v;
+    rmat_sample(scale, base, i, a, ab, abc, &u, &v);
+    const int64_t pu = pi[u], pv = pi[v];
+    if (pu == pv) continue;
+    int64_t p;
+    if (pu >= vb && pu < ve) {
+#pragma omp atomic capture
+      p = cur[pu - vb]++;
+      col[p] = (int32_t)pv;
+    }
+    if (pv >= vb && pv < ve) {
+#pragma omp atomic capture
+      p = cur[pv - vb]++;
+      col[p] = (int32_t)pu;
+    }
   }
   free(pi);
-  /* drop self loops: stable compaction (sequential, memory-bound) */
-  int64_t k = 0;
-  for (int64_t i = 0; i < ns; ++i) {
-    if (keep[i]) {
-      src[k] = src[2 * i]; dst[k] = dst[2 * i]; ++k;
-      src[k] = src[2 * i + 1]; dst[k] = dst[2 * i + 1]; ++k;
-    }
+  /* sort + dedupe every row in place; cur[v] = new degree */
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < nl; ++v) {
+    int32_t* r = col + off[v];
+    const int64_t len = off[v + 1] - off[v];
+    sort_row(r, len);
+    int64_t w = 0;
+    for (int64_t i = 0; i < len; ++i)
+      if (w == 0 || r[i] != r[w - 1]) r[w++] = r[i];
+    cur[v] = w;
   }
-  free(keep);
-  int rc = csr_from_arcs(n, src, dst, k, row_ptr_out, col_out, m_out);
-  free(src); free(dst);
+  int64_t* rp = (int64_t*)malloc(((size_t)nl + 1) * sizeof(int64_t));
+  if (!rp) { free(off); free(cur); free(col); return 2; }
+  prefix_sum(cur, rp, nl);
+  /* compact in place, ascending rows (rp[v] <= off[v], so a row never overwrites a later one) */
+  for (int64_t v = 0; v < nl; ++v)
+    if (rp[v] != off[v] && cur[v]) memmove(col + rp[v], col + off[v], (size_t)cur[v] * sizeof(int32_t));
+  const int64_t m = rp[nl];
+  int32_t* shrunk = (int32_t*)realloc(col, (size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  if (shrunk) col = shrunk;
+  free(off); free(cur);
+  *row_ptr_out = rp; *col_out = col; *m_out = m;
+  return 0;
+}
+
+int gen_rmat(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+             int64_t* n_out, int64_t* m_out, int64_t** row_ptr_out, int32_t** col_out) {
+  if (scale < 1 || scale > 30) return 1;
+  const int64_t n = (int64_t)1 << scale;
+  int rc = gen_rmat_range(scale, edge_factor, a, b, c, seed, 0, n, m_out, row_ptr_out, col_out);
   if (rc == 0) *n_out = n;
   return rc;
 }
