@@ -18,11 +18,16 @@
  *    detected with cudaPointerGetAttributes.  Host inputs are copied to the device and
  *    host outputs copied back inside the call.
  *  - Calls are synchronous: they return after every output is final (one stream sync).
+ *    The call's work is ordered after work already queued on opts->stream, or, when that is
+ *    NULL, after work already queued on the legacy default stream (an event on it is waited
+ *    for; the internal stream itself is non-blocking).
  *  - On error every scalar output is set to 0, array outputs are unspecified, nothing is
  *    thrown or aborted, and a human-readable detail is available from
  *    gc_last_error_message() (thread-local).
- *  - No global mutable state other than a per-device workspace memory pool; concurrent
- *    calls on distinct streams are allowed.
+ *  - No global mutable state other than a per-device workspace memory pool and per-device
+ *    attribute caches; no device- or context-wide setting (L2 limits, access-policy windows,
+ *    ...) is changed.  Concurrent calls on distinct streams are allowed.
+ *  - No tuning choice is read from the environment: they are all in gc_opts / gc_tuning.
  */
 #ifndef GC_H_
 #define GC_H_
@@ -33,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 1
+#define GC_ABI_VERSION 2
 
 typedef enum gc_status {
   GC_OK = 0,
@@ -95,6 +100,31 @@ typedef struct gc_work {
   uint64_t reserved[3];
 } gc_work;
 
+/* Schedule choices of the persistent kernel.  None of them changes the result (the colouring
+ * is a pure function of graph and policy); they exist for ablations and tests.  -1 (or 0 for
+ * state_bytes) = the measured default, stated per field. */
+typedef struct gc_tuning {
+  uint32_t struct_size;    /* = sizeof(gc_tuning) */
+  int32_t state_bytes;     /* 0: 8-bit state words with restarts to 16/32 bits; 2 or 4: start wider */
+  int32_t dense_div;       /* dense (id-order) rounds while |W_r| * dense_div > n; 0 = never dense;
+                              default 3.  A non-negative value also sets dense_div_n1 unless that
+                              is given explicitly */
+  int32_t dense_div_n1;    /* the same in dirty-set rounds; default 16 */
+  int32_t n1;              /* dirty-set rounds: 0 off, 1 when max degree <= 64 (default), 2 always */
+  int32_t list;            /* explicit list rounds: 0 off (default), 1 cost rule, 2 from round 3 */
+  int32_t compact;         /* dense Phase B lists pending vertices without marks: 0 (default) / 1 */
+  int32_t scatter_filter;  /* commit scatter skips committed neighbours: 0 (default) / 1 */
+  int32_t dch;             /* dense queue chunks of about n / (dch x warps) vertices; default 16 */
+  int32_t n1_chg;          /* mark only when chg(r-1) * n1_chg < |W_r|; 0 = every round (default) */
+  int32_t variant;         /* kernel: 0 = 4 CTAs/SM, 1 = 3 CTAs/SM (80 registers); -1 = chosen by a
+                              max-degree pre-pass (bounded degree <= 64 and m >= 8n -> 1) */
+  int32_t watchdog_ms;     /* device watchdog per grid barrier, ms (0 or -1: 60 000); tests use less */
+  int32_t reserved[4];
+} gc_tuning;
+
+/* Fill *t with "defaults" (-1 / 0 as above). */
+void gc_tuning_default(gc_tuning* t);
+
 typedef struct gc_opts {
   uint32_t struct_size;      /* = sizeof(gc_opts) (ABI check) */
   uint32_t policy;           /* gc_policy */
@@ -118,7 +148,8 @@ typedef struct gc_opts {
   uint64_t* phase_ns;        /* optional host pointer [2 * trace_capacity + 1] (diagnostics, with
                                 GC_FLAG_TRACE): device globaltimer (ns) after the ingest and
                                 after Phase A / Phase B of every round, persistent driver only */
-  uint64_t reserved[2];
+  const gc_tuning* tuning;   /* optional schedule overrides (NULL = measured defaults) */
+  uint64_t reserved[1];
 } gc_opts;
 
 /* Fill *o with the defaults above (policy HIGHER_ID, flags GC_FLAG_VALIDATE). */

@@ -1,33 +1,35 @@
 /*
- * gc_dist.h — vertex-range partitioned SGR colouring (multi-GPU path), C ABI.
- * Library: paper_1606_06025_b200/csrc/libgc.so (same library as gc.h).
+ * gc_dist.h — multi-GPU SGR colouring, one rank per GPU (C ABI; same library as gc.h:
+ * paper_1606_06025_b200/csrc/libgc.so).  These are SURVEY §8(b)'s multi-GPU calls.
  *
- * SURVEY §8(e) / BASELINE north star: "The 8-GPU path partitions the graph by vertex range
- * with edge-balanced splits and ghost colors.  Each round, changed boundary colors are
- * exchanged ... and cross-partition conflicts are resolved by global id.  The result must
- * be bit-identical to 1 GPU."
+ * What is computed: exactly gc_color's colouring (Alg. 7 Data-GC, with
+ * FirstFit Alg. 4 PAPER.md:327-338 and ConflictResolve Alg. 5, in Jacobi
+ * rounds).  The graph is partitioned by vertex range (BASELINE north star: "The 8-GPU path
+ * partitions the graph by vertex range with edge-balanced splits and ghost colors ... cross-
+ * partition conflicts are resolved by global id.  The result must be bit-identical to 1 GPU");
+ * every cover of [0, n) gives bit-identical colours, num_colors, rounds and |W_r| trace.
  *
- * One partition per process/GPU.  A partition holds the rows [v_begin, v_end) of the global
- * CSR (row_ptr_local = row_ptr[v_begin..v_end] - row_ptr[v_begin], col_idx_local in GLOBAL
- * ids) and a replicated state word per global vertex.  The caller drives the rounds and
- * moves the packed (vertex, word) pairs between partitions (all-gather; the Python driver
- * paper_1606_06025_b200.dist does it with torch.distributed / NCCL):
+ * How (device-initiated exchange): every rank runs ONE persistent kernel for
+ * the whole colouring — the paper's kernel fusion with a global barrier
+ * taken across GPUs.  Each rank holds full-size replicas of the per-vertex state words,
+ * forbidden-colour planes, dirty marks and (DEGREE) degrees in a window that every other rank
+ * maps through CUDA IPC (NVLink peer memory).  Inside the kernel:
+ *   - a changed tentative colour or a commit of a boundary vertex is stored straight into the
+ *     replicas of the ranks that hold it as a ghost;
+ *   - a winner ORs its colour bit into the owner's plane byte of every neighbour (peer RED);
+ *   - dirty marks of successors across the cut are peer byte stores;
+ *   - the two grid barriers per round span every rank's grid (system-scope fence, one flag per
+ *     rank pair), and the barrier leader adds the rank's |W_{r+1}| into every rank's global
+ *     count, so every rank leaves the round loop at the same round with no host involvement.
+ * NCCL (loaded from libnccl.so.2 at run time) only bootstraps: it all-gathers the ranks'
+ * ranges, arguments and IPC handles once per call (handles only when a window grows).
  *
- *   create;  loop { phase_a; pack(0) -> all-gather -> unpack;          (round >= 2)
- *                   phase_b(&local_next); pack(1) -> all-gather -> unpack;
- *                   if sum over partitions of local_next == 0: break; next_round }
- *   finalize; destroy
- *
- * Round r reads exactly the state the single-GPU path reads (Jacobi rounds, reading C2), so
- * the colours are bit-identical to gc_color for every cover of [0, n).
- * First-Fit is incremental as on one GPU: each partition keeps forbidden-colour planes for its
- * own vertices; local winners OR their colour into them directly, and the commit pairs of
- * remote winners are applied through a halo adjacency (for every remote vertex, its local
- * neighbours) built by gc_dist_create.  Only boundary vertices (with a remote neighbour) are
- * packed: no other partition ever reads the others' words.  Policies HIGHER_ID
- * and LOWER_ID (global ids decide); DEGREE is single-GPU only (GC_ERR_UNSUPPORTED).
- * All pointers are device memory of opts->device; every call is synchronous on the
- * partition's internal stream.  Errors: see gc.h conventions.
+ * Ownership and errors: as in gc.h.  Every call of gc_color_dist is collective: all ranks of
+ * the communicator call it with the same n_global, policy, flags and max_rounds, and their
+ * [v_begin, v_end) ranges, in rank order, must tile [0, n_global); otherwise every rank returns
+ * GC_ERR_INVALID_ARGUMENT.  A failure on any rank (allocation, validation) is agreed by all
+ * ranks before any kernel starts, so no rank is left waiting.  A device-side watchdog
+ * (60 s per barrier) turns a lost rank into GC_ERR_CUDA and marks the communicator unusable.
  */
 #ifndef GC_DIST_H_
 #define GC_DIST_H_
@@ -37,29 +39,50 @@
 extern "C" {
 #endif
 
-typedef struct gc_dist gc_dist;
+#define GC_MAX_RANKS 8
+#define GC_NCCL_UNIQUE_ID_BYTES 128
 
-/* Allocate the partition state (replicated state words: 4 B x n_global; forbidden-colour
- * planes; halo adjacency, 4 B per cut edge) from the device's stream-ordered pool and build W_1. */
-gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64_t v_end,
-                         const int64_t* row_ptr_local, const int32_t* col_idx_local,
-                         const gc_opts* opts);
-/* Phase A (FirstFit) of the local pending vertices; no-op in round 1. */
-gc_status gc_dist_phase_a(gc_dist* h);
-/* Phase B (ConflictResolve + push); *local_next = local |W_{r+1}|. */
-gc_status gc_dist_phase_b(gc_dist* h, uint32_t* local_next);
-/* what 0: (v, word) of the local pending boundary vertices (after Phase A); what 1: the local
- * boundary winners (after Phase B).  pairs: device, >= 2*(v_end-v_begin) uint32; *count =
- * pairs written. */
-gc_status gc_dist_pack(gc_dist* h, int32_t what, uint32_t* pairs, uint64_t* count);
-/* Write gathered (v, word) pairs into the replicated state; committed words of remote
- * vertices also set their colour bit in the planes of their local neighbours (halo). */
-gc_status gc_dist_unpack(gc_dist* h, const uint32_t* pairs, uint64_t count);
-/* W_{r+1} becomes the input worklist of round r+1. */
-gc_status gc_dist_next_round(gc_dist* h);
-/* colors_local (device, [v_end-v_begin]); *max_color_local; *rounds = the current round. */
-gc_status gc_dist_finalize(gc_dist* h, uint32_t* colors_local, uint32_t* max_color_local, uint32_t* rounds);
-gc_status gc_dist_destroy(gc_dist* h);
+typedef struct gc_comm gc_comm;
+
+/* ncclGetUniqueId into id_out[GC_NCCL_UNIQUE_ID_BYTES] (call on one rank, broadcast the bytes,
+ * e.g. with torch.distributed).  GC_ERR_NCCL when libnccl.so.2 cannot be loaded. */
+gc_status gc_nccl_unique_id(void* id_out);
+
+/* Collective over `world` processes (1 <= world <= GC_MAX_RANKS): ncclCommInitRank on `device`
+ * (-1 = current).  The communicator owns a stream and, after the first gc_color_dist, the
+ * rank's IPC window (about 74 bytes per global vertex). */
+gc_status gc_comm_init(gc_comm** out, int32_t rank, int32_t world, const void* nccl_unique_id,
+                       int32_t device);
+
+/* One-process emulation (tests, one GPU): comms_out[world] communicators whose ranks all live
+ * on `device` and bootstrap through memory instead of NCCL.  The kernels, windows, peer stores
+ * and cross-rank barriers are the multi-GPU ones; each rank's gc_color_dist must be called
+ * concurrently from its own host thread (the ranks' persistent kernels run side by side, each
+ * on 1/world of the SMs).  The ranks' streams must not share a hardware queue: world > 1 needs
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 x world in the environment before CUDA initialises
+ * (else GC_ERR_UNSUPPORTED). */
+gc_status gc_comm_init_local(gc_comm** comms_out, int32_t world, int32_t device);
+
+/*
+ * gc_color_dist — colour the rows [v_begin, v_end) owned by this rank.
+ *   n_global          number of vertices of the whole graph (<= INT32_MAX).
+ *   row_ptr_local     int64[v_end - v_begin + 1]: row_ptr[v_begin..v_end] - row_ptr[v_begin].
+ *   col_idx_local     int32[row_ptr_local[v_end - v_begin]]: the rows' neighbours, GLOBAL ids,
+ *                     sorted, loop-free, symmetric graph (GC_FLAG_VALIDATE checks range, order,
+ *                     loops of the local rows; GC_FLAG_VALIDATE_SYMMETRY is rejected).
+ *   opts              as gc_color (policy, flags GC_FLAG_VALIDATE / _TRACE / _COUNT_WORK, trace,
+ *                     stream, kernel_ms, tuning); GC_FLAG_PULL_FIRSTFIT and GC_FLAG_HOST_ROUNDS
+ *                     are rejected.  opts->device is ignored (the communicator's device).
+ *   colors_out_local  uint32[v_end - v_begin], host or device.
+ *   num_colors, rounds   global values, identical on every rank (trace: the global |W_r|).
+ */
+gc_status gc_color_dist(gc_comm* c, int64_t n_global, int64_t v_begin, int64_t v_end,
+                        const int64_t* row_ptr_local, const int32_t* col_idx_local,
+                        const gc_opts* opts, uint32_t* colors_out_local, uint32_t* num_colors,
+                        uint32_t* rounds);
+
+/* Release the window, peer mappings, stream and NCCL communicator (NULL: no-op). */
+gc_status gc_comm_destroy(gc_comm* c);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,15 @@ class Work(ctypes.Structure):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}
 
 
+class Tuning(ctypes.Structure):
+    """gc_tuning (include/gc.h): schedule overrides; -1 = measured default."""
+    _fields_ = [("struct_size", ctypes.c_uint32), ("state_bytes", ctypes.c_int32),
+                ("dense_div", ctypes.c_int32), ("dense_div_n1", ctypes.c_int32), ("n1", ctypes.c_int32),
+                ("list", ctypes.c_int32), ("compact", ctypes.c_int32), ("scatter_filter", ctypes.c_int32),
+                ("dch", ctypes.c_int32), ("n1_chg", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("watchdog_ms", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
 class Opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("policy", ctypes.c_uint32),
                 ("flags", ctypes.c_uint32), ("max_rounds", ctypes.c_uint32),
@@ -62,12 +71,15 @@ class Opts(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("trace_worklist", ctypes.c_void_p),
                 ("trace_capacity", ctypes.c_uint32), ("group_bin_max", ctypes.c_uint32),
                 ("work", ctypes.POINTER(Work)), ("kernel_ms", ctypes.POINTER(ctypes.c_float)),
-                ("phase_ns", ctypes.c_void_p), ("reserved", ctypes.c_uint64 * 2)]
+                ("phase_ns", ctypes.c_void_p), ("tuning", ctypes.POINTER(Tuning)),
+                ("reserved", ctypes.c_uint64 * 1)]
 
 
 _vp = ctypes.c_void_p
 _lib.gc_opts_default.argtypes = [ctypes.POINTER(Opts)]
 _lib.gc_opts_default.restype = None
+_lib.gc_tuning_default.argtypes = [ctypes.POINTER(Tuning)]
+_lib.gc_tuning_default.restype = None
 _lib.gc_color.argtypes = [ctypes.c_int64, _vp, _vp, ctypes.POINTER(Opts), _vp,
                           ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]
 _lib.gc_color.restype = ctypes.c_int
@@ -83,6 +95,7 @@ _lib.gc_abi_version.argtypes = []
 _lib.gc_abi_version.restype = ctypes.c_int32
 
 assert ctypes.sizeof(Opts) == 96, ctypes.sizeof(Opts)
+assert ctypes.sizeof(Tuning) == 64, ctypes.sizeof(Tuning)
 
 
 def _err(status: int):
@@ -119,12 +132,25 @@ def default_opts() -> Opts:
     return o
 
 
+def make_tuning(tuning: dict | None):
+    """gc_tuning from a dict of its field names (None -> NULL: the measured defaults)."""
+    if not tuning:
+        return None
+    t = Tuning()
+    _lib.gc_tuning_default(ctypes.byref(t))
+    for k, v in tuning.items():
+        if k not in dict(Tuning._fields_) or k in ("struct_size", "reserved"):
+            raise ValueError(f"unknown gc_tuning field {k!r}")
+        setattr(t, k, int(v))
+    return t
+
+
 def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
           symmetry: bool = False, pull_firstfit: bool = False, host_rounds: bool = False,
           trace: bool = False, count_work: bool = False, max_rounds: int = 0,
           thread_bin_max: int = 0, group_bin_max: int = 0, warp_bin_max: int = 0, blocks_per_sm: int = 0,
           stream=None, device: int | None = None, out=None, time_kernel: bool = False,
-          phase_times: bool = False) -> ColorResult:
+          phase_times: bool = False, tuning: dict | None = None) -> ColorResult:
     """gc_color(n, row_ptr, col_idx, opts, colors_out, &num_colors, &rounds) (include/gc.h).
 
     row_ptr: int64[n+1], col_idx: int32[m] — torch tensors (CUDA or CPU) or numpy arrays.
@@ -144,6 +170,9 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
     o.warp_bin_max = warp_bin_max
     o.group_bin_max = group_bin_max
     o.blocks_per_sm = blocks_per_sm
+    tun = make_tuning(tuning)
+    if tun is not None:
+        o.tuning = ctypes.pointer(tun)
     dev_inputs = _is_cuda(row_ptr)
     if dev_inputs:
         import torch

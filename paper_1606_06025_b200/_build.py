@@ -1,23 +1,33 @@
-"""Build (nvcc, sm_100a) and load the in-tree CUDA library ``csrc/libgc.so``."""
+"""Build (nvcc, sm_100a) and load the in-tree CUDA library ``csrc/libgc.so``.
+
+Every ``csrc/*.cu`` is compiled to an object in parallel (the persistent kernel instances are
+split by state-word width into ``inst_*.cu``), then linked into one shared library.
+"""
 from __future__ import annotations
 
 import ctypes
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(CSRC, "obj")
 LIB_PATH = os.path.join(CSRC, "libgc.so")
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-diag-suppress", "128"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "128"]
 
 
-def _sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+def _headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
+
+
+def _units():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
 def _nvcc() -> str:
@@ -27,17 +37,31 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+def _stale(target, deps):
+    return not os.path.exists(target) or any(os.path.getmtime(target) < os.path.getmtime(d) for d in deps)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/gc_api.cu (+ headers) into csrc/libgc.so for sm_100a."""
-    srcs = _sources()
-    if (not force and os.path.exists(LIB_PATH)
-            and all(os.path.getmtime(LIB_PATH) >= os.path.getmtime(s) for s in srcs)):
+    """Compile csrc/*.cu (+ headers) into csrc/libgc.so for sm_100a."""
+    units, headers = _units(), _headers()
+    if not force and not _stale(LIB_PATH, units + headers):
         return LIB_PATH
+    os.makedirs(OBJ, exist_ok=True)
+    nvcc = _nvcc()
+
+    def compile_unit(src):
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        if force or _stale(obj, [src] + headers):
+            tmp = obj + f".tmp{os.getpid()}"
+            cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", tmp, src]
+            subprocess.check_call(cmd)
+            os.replace(tmp, obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(units), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_unit, units))
     tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "gc_api.cu")]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

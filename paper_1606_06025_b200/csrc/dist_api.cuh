@@ -1,428 +1,694 @@
-// dist_api.cuh — vertex-range partitioned SGR (multi-GPU path, include/gc_dist.h).
-// Included at the end of gc_api.cu (same translation unit: shares its host helpers).
+// dist_api.cuh — host side of include/gc_dist.h: multi-GPU SGR with a device-initiated
+// exchange.  Included at the end of gc_api.cu (same translation unit: shares
+// its host helpers and the persistent kernel instances).
 //
-// One partition = one process/GPU holding the rows [v_begin, v_end) (row_ptr rebased to 0,
-// col_idx in global ids) and a REPLICATED state word per global vertex (ghost colours).
-// The round structure of the single-GPU path is kept; between the phases the caller
-// exchanges packed (vertex, state word) pairs with the other partitions (NCCL all-gather over
-// NVLink via torch.distributed, see paper_1606_06025_b200/dist.py):
-//   round r:  [Phase A: tentative colours of the local pending vertices, pull First-Fit over
-//              the replicated committed colours]  -> exchange the local pending tents
-//             Phase B: conflict scan against the replicated tents, global ids decide
-//              -> exchange the local winners (committed words) ; global |W| decides the end.
-// Every partition therefore sees exactly the single-GPU state after each phase, so the
-// colouring is bit-identical to one GPU for any cover of [0, n).
+// Per rank: one IPC-exportable window (cudaMalloc) laid out identically on every rank for a
+// given n_global (WinLayout); every rank maps every other rank's window once (CUDA IPC, or
+// plain pointers in the one-process emulation) and the persistent kernel receives the table of
+// peer pointers (Params::peer).  NCCL is used only to all-gather small host records
+// (arguments, IPC handles) — the bootstrap; the colouring itself never returns to the host.
 #pragma once
-#include <cub/device/device_scan.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
-namespace gcdev {
+#include <condition_variable>
+#include <mutex>
+#include <vector>
 
-__global__ void __launch_bounds__(BLOCK) k_fill_u32(uint32_t* p, int64_t n, uint32_t v) {
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) p[i] = v;
-}
+namespace {
 
-// (vertex, state word) of every entry of the given worklist bins; with only_committed the
-// entries whose word has the commit bit (this round's winners).
-__global__ void __launch_bounds__(BLOCK) k_pack(const WE* W, const uint32_t* off, const uint32_t* cnt,
-                                                const uint32_t* st, int only_committed, uint32_t* out,
-                                                unsigned long long* out_count, const uint8_t* boundary,
-                                                int32_t v_base) {
-  const int lane = threadIdx.x & 31;
-  for (int b = 0; b < NBIN; ++b) {
-    const uint32_t nb = cnt[b];
-    const WE* Wb = W + off[b];
-    for (uint32_t base = (blockIdx.x * BLOCK) + (threadIdx.x & ~31u); base < nb; base += gridDim.x * BLOCK) {
-      const uint32_t i = base + lane;
-      bool take = false;
-      int32_t v = 0;
-      uint32_t s = 0;
-      if (i < nb) {
-        v = ldw_v(Wb + i);
-        s = lds(st + v);
-        take = boundary[v - v_base] && (!only_committed || (s & SW<uint32_t>::COMMIT));
-      }
-      const unsigned m = __ballot_sync(FULL, take);
-      if (!m) continue;
-      unsigned long long pos = 0;
-      if (lane == __ffs(m) - 1) pos = atomicAdd(out_count, (unsigned long long)__popc(m));
-      pos = __shfl_sync(FULL, pos, __ffs(m) - 1);
-      if (take) {
-        const unsigned long long j = pos + __popc(m & lanemask_lt());
-        out[2 * j] = (uint32_t)v;
-        out[2 * j + 1] = s;
-      }
+// ---- NCCL, resolved at run time (the process may already hold torch's libnccl.so.2)
+struct NcclApi {
+  bool ok = false;
+  char why[256] = "";
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi* nccl_api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      snprintf(a.why, sizeof(a.why), "dlopen(libnccl.so.2): %s", dlerror());
+      return;
     }
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+    if (!a.ok) snprintf(a.why, sizeof(a.why), "libnccl.so.2 lacks a required symbol");
+  });
+  return &a;
+}
+
+// ---- one-process emulation: ranks are threads; the bootstrap all-gather is a memory exchange
+// behind a generation barrier (two slot sets by generation parity, so a fast rank entering the
+// next exchange never overwrites a slot a slow rank is still copying).
+struct LocalGroup {
+  int world = 0;
+  int refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<std::vector<uint8_t>> slot[2];
+};
+
+constexpr size_t kBootBytes = 256;  // largest bootstrap record
+
+// Window layout (byte offsets), identical on every rank for a given n_global.
+struct WinLayout {
+  int64_t pitch = 0;
+  uint32_t np = 0;
+  size_t xflag = 0, peers = 0, info = 0, st = 0, planes = 0, dirty = 0, ksplit = 0, bmask = 0, total = 0;
+};
+WinLayout win_layout(int64_t n_global) {
+  WinLayout L;
+  L.pitch = (n_global + 255) / 256 * 256;
+  if (L.pitch == 0) L.pitch = 256;
+  L.np = (uint32_t)MAX_PLANES;
+  if ((uint64_t)L.np * (uint64_t)L.pitch > (16ull << 30)) {
+    const uint64_t fit = (16ull << 30) / (uint64_t)L.pitch;
+    L.np = fit < 16 ? 16u : (uint32_t)fit;
   }
+  const size_t P = (size_t)L.pitch;
+  L.xflag = 0;                                        // [MAX_RANKS][32] u32, persistent
+  L.peers = 2048;                                     // Peer[MAX_RANKS], written per call
+  static_assert(MAX_RANKS * 32 * 4 <= 2048 && MAX_RANKS * sizeof(Peer) <= 2048, "window header");
+  L.info = 4096;                                      // DevInfo, zeroed per launch
+  L.st = L.info + ((sizeof(DevInfo) + 4095) / 4096) * 4096;  // up to 4-byte words
+  L.planes = L.st + 4 * P;
+  L.dirty = L.planes + (size_t)L.np * P;
+  L.ksplit = L.dirty + P;
+  L.bmask = L.ksplit + 4 * P;
+  L.total = L.bmask + P;
+  return L;
 }
 
-__global__ void __launch_bounds__(BLOCK) k_unpack(const uint32_t* pairs, int64_t count, uint32_t* st) {
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < count; i += (int64_t)gridDim.x * BLOCK)
-    st[pairs[2 * i]] = pairs[2 * i + 1];
-}
+}  // namespace
 
-// Halo adjacency (push First-Fit across partitions): for every remote vertex w, the local
-// vertices adjacent to it (the symmetric half of the cut edges), as offsets hoff[w] into hadj.
-// A remote winner's colour bit reaches the forbidden-colour planes of its local neighbours
-// through this list when its commit pair is unpacked (the winner's own partition cannot RED
-// into another GPU's planes).
-// One warp per local vertex (coalesced row reads; hub rows do not serialise one thread).
-__global__ void __launch_bounds__(BLOCK) k_halo_count(Params p, int64_t n_local, int64_t v_begin, int64_t v_end,
-                                                      uint32_t* hcnt, uint8_t* boundary) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * BLOCK) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < n_local; u += nw) {
-    bool b = false;
-    for (int64_t e = p.rp[u] + lane; e < p.rp[u + 1]; e += 32) {
-      const int32_t w = p.ci[e];
-      if (w < v_begin || w >= v_end) {
-        atomicAdd(&hcnt[w], 1u);
-        b = true;
-      }
-    }
-    b = __any_sync(FULL, b);
-    if (lane == 0) boundary[u] = b ? 1 : 0;  // only boundary vertices' words are read remotely
-  }
-}
-__global__ void __launch_bounds__(BLOCK) k_halo_fill(Params p, int64_t n_local, int64_t v_begin, int64_t v_end,
-                                                     uint32_t* hcur, int32_t* hadj) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * BLOCK) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < n_local; u += nw)
-    for (int64_t e = p.rp[u] + lane; e < p.rp[u + 1]; e += 32) {
-      const int32_t w = p.ci[e];
-      if (w < v_begin || w >= v_end) hadj[atomicAdd(&hcur[w], 1u)] = (int32_t)(v_begin + u);
-    }
-}
-// Commit pairs of remote winners -> colour bit into the planes of their local neighbours.
-__global__ void __launch_bounds__(BLOCK) k_halo_apply(const uint32_t* pairs, int64_t count, int64_t v_begin,
-                                                      int64_t v_end, const uint32_t* hoff, const int32_t* hadj,
-                                                      uint8_t* fmp, int64_t plane, uint32_t np) {
-  const int64_t T = (int64_t)gridDim.x * BLOCK;
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < count; i += T) {
-    const uint32_t w = pairs[2 * i], word = pairs[2 * i + 1];
-    if (!(word & SW<uint32_t>::COMMIT) || ((int64_t)w >= v_begin && (int64_t)w < v_end)) continue;
-    const uint32_t c = word & SW<uint32_t>::CMASK;
-    if (c == 0 || c > 8u * np) continue;
-    uint8_t* pl = fmp + (int64_t)((c - 1) >> 3) * plane;
-    const uint32_t bit = 1u << ((c - 1) & 7);
-    for (uint32_t j = hoff[w]; j < hoff[w + 1]; ++j) red_plane<uint32_t>(pl, hadj[j], bit);
-  }
-}
-
-}  // namespace gcdev
-
-struct gc_dist {
-  int dev = 0;
-  cudaStream_t stream = nullptr;
-  int grid = 0;
-  int policy = 0;
-  uint32_t round = 1;
-  uint32_t max_rounds = 0;
-  int64_t n_global = 0, v_begin = 0, v_end = 0;
-  Params p;
-  WE* W[2] = {nullptr, nullptr};
-  int cur = 0;                       // W[cur] = W_in of the current round
-  uint32_t cnt_in[NBIN] = {0, 0};    // |W_in| per bin
-  uint32_t off[NBIN] = {0, 0};
-  uint32_t* d_off = nullptr;         // device copies for k_pack
-  uint32_t* d_cnt = nullptr;
-  unsigned long long* d_count = nullptr;
-  void* mem[16] = {};
-  uint8_t* boundary = nullptr;       // local vertices with a remote neighbour (the only ones packed)
-  uint32_t* hoff = nullptr;          // halo adjacency (push First-Fit across partitions)
-  int32_t* hadj = nullptr;
-  int nmem = 0;
+struct gc_comm {
+  int rank = 0, world = 1, dev = 0;
+  ncclComm_t nccl = nullptr;
+  LocalGroup* lg = nullptr;
+  cudaStream_t stream = nullptr;   // non-blocking; each call waits for the legacy stream's prior work
+  void* boot = nullptr;            // NCCL bootstrap scratch: send [kBootBytes] + recv [world x kBootBytes]
+  uint8_t* win = nullptr;          // this rank's window (cudaMalloc, IPC-exportable)
+  size_t win_bytes = 0;
+  uint8_t* peer[MAX_RANKS] = {};   // every rank's window in this process's address space
+  bool mapped[MAX_RANKS] = {};     // peer[q] is an IPC mapping to close
+  uint32_t epoch = 0;              // cross-rank barrier epochs used so far (same on every rank)
+  DevInfo* hinfo = nullptr;        // pinned: read back after a launch without a staging copy
+  bool broken = false;
 };
 
 namespace {
 
-gc_status dist_fail(gc_dist* h, cudaError_t e, const char* what) {
-  (void)h;
-  return cuda_fail(e, what);
+gc_status nccl_fail(ncclResult_t r, const char* what) {
+  set_err("%s: %s", what, nccl_api()->GetErrorString ? nccl_api()->GetErrorString(r) : "NCCL error");
+  return GC_ERR_NCCL;
 }
 
-#define DK(call)                                                \
-  do {                                                          \
-    cudaError_t e_ = (call);                                    \
-    if (e_ != cudaSuccess) return dist_fail(h, e_, #call);      \
-  } while (0)
+// All-gather `bytes` (<= kBootBytes) per rank from every rank into all[world * bytes] (host).
+gc_status boot_allgather(gc_comm* c, const void* mine, size_t bytes, void* all) {
+  if (c->lg) {
+    LocalGroup* g = c->lg;
+    std::unique_lock<std::mutex> lk(g->mu);
+    const uint64_t my_gen = g->gen;
+    auto& slots = g->slot[my_gen & 1];
+    slots[c->rank].assign((const uint8_t*)mine, (const uint8_t*)mine + bytes);
+    if (++g->arrived == g->world) {
+      g->arrived = 0;
+      ++g->gen;
+      g->cv.notify_all();
+    } else {
+      g->cv.wait(lk, [&] { return g->gen != my_gen; });
+    }
+    for (int q = 0; q < c->world; ++q) memcpy((uint8_t*)all + q * bytes, slots[q].data(), bytes);
+    return GC_OK;
+  }
+  NcclApi* a = nccl_api();
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(c->boot, mine, bytes, cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return cuda_fail(e, "bootstrap H2D");
+  uint8_t* recv = (uint8_t*)c->boot + kBootBytes;
+  ncclResult_t r = a->AllGather(c->boot, recv, bytes, ncclUint8, c->nccl, c->stream);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  if ((e = cudaMemcpyAsync(all, recv, bytes * c->world, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(e, "bootstrap D2H");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(e, "bootstrap sync");
+  return GC_OK;
+}
 
-void launch_dist_b(gc_dist* h, int grid, const Params& p, uint32_t r, WE* W, WE* Wo) {
-  if (h->policy == HIGHER_ID) k_phase_b<HIGHER_ID, true, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
-  else k_phase_b<LOWER_ID, true, false><<<grid, BLOCK, 0, h->stream>>>(p, r, W, Wo);
+// Agree on a status: every rank returns the worst (largest code) of all ranks' statuses.
+gc_status agree(gc_comm* c, gc_status mine) {
+  int32_t all[MAX_RANKS] = {};
+  const int32_t m = (int32_t)mine;
+  gc_status s = boot_allgather(c, &m, sizeof(m), all);
+  if (s != GC_OK) {
+    c->broken = true;
+    return s;
+  }
+  gc_status worst = GC_OK;
+  int who = -1;
+  for (int q = 0; q < c->world; ++q)
+    if (all[q] > (int32_t)worst) { worst = (gc_status)all[q]; who = q; }
+  if (worst != GC_OK && mine == GC_OK) set_err("gc_color_dist: rank %d failed with %s", who, gc_status_string(worst));
+  return worst;
+}
+
+void close_window(gc_comm* c) {
+  for (int q = 0; q < MAX_RANKS; ++q) {
+    if (c->mapped[q]) cudaIpcCloseMemHandle(c->peer[q]);
+    c->mapped[q] = false;
+    c->peer[q] = nullptr;
+  }
+  if (c->win) cudaFree(c->win);
+  c->win = nullptr;
+  c->win_bytes = 0;
+}
+
+// Make every rank's window hold `need` bytes and map the peers' windows (collective).
+gc_status ensure_window(gc_comm* c, size_t need) {
+  // every rank sees the same `need` (same n_global), so all decide alike
+  if (c->win && c->win_bytes >= need) return GC_OK;
+  close_window(c);
+  gc_status mine = GC_OK;
+  const size_t bytes = (need + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+  cudaError_t e = cudaMalloc((void**)&c->win, bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->win, 0, bytes);  // flags start at epoch 0
+  if (e != cudaSuccess) {
+    mine = cuda_fail(e, "gc_color_dist: window cudaMalloc");
+    c->win = nullptr;
+  } else {
+    c->win_bytes = bytes;
+  }
+  c->epoch = 0;
+  struct Rec {
+    int32_t status;
+    int32_t pad;
+    uint64_t ptr;
+    cudaIpcMemHandle_t h;
+  } rec, all[MAX_RANKS];
+  memset(&rec, 0, sizeof(rec));
+  rec.status = (int32_t)mine;
+  rec.ptr = (uint64_t)(uintptr_t)c->win;
+  if (!c->lg && c->win && c->world > 1) {
+    e = cudaIpcGetMemHandle(&rec.h, c->win);
+    if (e != cudaSuccess) rec.status = (int32_t)cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(Rec) <= kBootBytes, "bootstrap record");
+  gc_status s = boot_allgather(c, &rec, sizeof(rec), all);
+  if (s != GC_OK) return s;
+  gc_status worst = GC_OK;
+  for (int q = 0; q < c->world; ++q)
+    if (all[q].status > (int32_t)worst) worst = (gc_status)all[q].status;
+  if (worst == GC_OK) {
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) {
+        c->peer[q] = c->win;
+      } else if (c->lg) {
+        c->peer[q] = (uint8_t*)(uintptr_t)all[q].ptr;
+      } else {
+        void* ptr = nullptr;
+        e = cudaIpcOpenMemHandle(&ptr, all[q].h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          worst = cuda_fail(e, "cudaIpcOpenMemHandle");
+          break;
+        }
+        c->peer[q] = (uint8_t*)ptr;
+        c->mapped[q] = true;
+      }
+    }
+  }
+  worst = agree(c, worst);  // a failed mapping anywhere: every rank drops its window
+  if (worst != GC_OK) close_window(c);
+  return worst;
 }
 
 }  // namespace
 
 extern "C" {
 
-gc_status gc_dist_create(gc_dist** out, int64_t n_global, int64_t v_begin, int64_t v_end,
-                         const int64_t* row_ptr_local, const int32_t* col_idx_local, const gc_opts* opts_in) {
+gc_status gc_nccl_unique_id(void* id_out) {
   g_err[0] = 0;
-  if (!out) {
-    set_err("gc_dist_create: out is NULL");
+  if (!id_out) {
+    set_err("gc_nccl_unique_id: NULL id_out");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  NcclApi* a = nccl_api();
+  if (!a->ok) {
+    set_err("gc_nccl_unique_id: %s", a->why);
+    return GC_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  ncclResult_t r = a->GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  static_assert(sizeof(id) == GC_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  memcpy(id_out, &id, sizeof(id));
+  return GC_OK;
+}
+
+static gc_status comm_common(gc_comm* c, int32_t device) {
+  int prev = 0;
+  cudaError_t e = cudaGetDevice(&prev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  c->dev = device >= 0 ? device : prev;
+  if ((e = cudaSetDevice(c->dev)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  DevFacts f;
+  if ((e = dev_facts(c->dev, &f)) != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "dev_facts"); }
+  if (f.major != 10 || !f.coop) {
+    cudaSetDevice(prev);
+    set_err("gc_comm: device %d is not an sm_100-class device with cooperative launch", c->dev);
+    return GC_ERR_UNSUPPORTED;
+  }
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->hinfo, sizeof(DevInfo), cudaHostAllocDefault);
+  if (e == cudaSuccess && !c->lg) e = cudaMalloc(&c->boot, kBootBytes * (1 + MAX_RANKS));
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "gc_comm: stream / bootstrap buffer");
+  return GC_OK;
+}
+
+gc_status gc_comm_init(gc_comm** out, int32_t rank, int32_t world, const void* nccl_unique_id, int32_t device) {
+  g_err[0] = 0;
+  if (!out || !nccl_unique_id || world < 1 || world > MAX_RANKS || rank < 0 || rank >= world) {
+    set_err("gc_comm_init: invalid argument (world must be 1..%d, 0 <= rank < world)", MAX_RANKS);
     return GC_ERR_INVALID_ARGUMENT;
   }
   *out = nullptr;
-  gc_opts o;
-  gc_opts_default(&o);
-  if (opts_in) {
-    if (opts_in->struct_size != sizeof(gc_opts)) {
-      set_err("gc_dist_create: bad opts->struct_size");
-      return GC_ERR_INVALID_ARGUMENT;
-    }
-    o = *opts_in;
+  NcclApi* a = nccl_api();
+  if (!a->ok) {
+    set_err("gc_comm_init: %s", a->why);
+    return GC_ERR_NCCL;
   }
-  if (n_global < 0 || n_global > INT32_MAX || v_begin < 0 || v_end < v_begin || v_end > n_global) {
-    set_err("gc_dist_create: bad range [%lld, %lld) of n=%lld", (long long)v_begin, (long long)v_end,
-            (long long)n_global);
-    return GC_ERR_INVALID_ARGUMENT;
-  }
-  if (o.policy == GC_POLICY_DEGREE) {
-    set_err("gc_dist_create: GC_POLICY_DEGREE is single-GPU only (needs remote degrees)");
-    return GC_ERR_UNSUPPORTED;
-  }
-  if (o.policy > GC_POLICY_DEGREE) {
-    set_err("gc_dist_create: unknown policy %u", o.policy);
-    return GC_ERR_INVALID_ARGUMENT;
-  }
-  const int64_t nl = v_end - v_begin;
-  if (nl > 0 && (!row_ptr_local || !col_idx_local)) {
-    set_err("gc_dist_create: NULL row_ptr/col_idx");
-    return GC_ERR_INVALID_ARGUMENT;
-  }
-  if ((nl > 0 && is_device_ptr(row_ptr_local) != 1) || (nl > 0 && is_device_ptr(col_idx_local) != 1)) {
-    set_err("gc_dist_create: row_ptr_local and col_idx_local must be device memory");
-    return GC_ERR_INVALID_ARGUMENT;
-  }
-  gc_dist* h = new gc_dist();
+  gc_comm* c = new gc_comm();
+  c->rank = rank;
+  c->world = world;
+  gc_status s = comm_common(c, device);
+  if (s != GC_OK) { gc_comm_destroy(c); return s; }
   int prev = 0;
   cudaGetDevice(&prev);
-  h->dev = o.device >= 0 ? o.device : prev;
-  cudaError_t e = cudaSetDevice(h->dev);
-  if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaSetDevice"); }
-  DevFacts f;
-  if ((e = dev_facts(h->dev, &f)) != cudaSuccess) { delete h; return cuda_fail(e, "dev_facts"); }
-  if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess) { delete h; return cuda_fail(e, "stream"); }
-  h->grid = f.sms * 4;
-  h->policy = (int)o.policy;
-  h->n_global = n_global;
-  h->v_begin = v_begin;
-  h->v_end = v_end;
-  h->max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)(n_global + 1 > 0xffffffffLL ? 0xffffffffu : n_global + 1);
-  // workspace from the per-device stream-ordered pool (cached across partitions: creating
-  // and destroying a partition per colouring costs no cudaMalloc/cudaFree)
-  cudaMemPool_t pool;
-  if ((e = get_pool(h->dev, &pool)) != cudaSuccess) { gc_dist_destroy(h); return cuda_fail(e, "get_pool"); }
-  auto alloc = [&](void** q, size_t bytes) {
-    cudaError_t ee = cudaMallocFromPoolAsync(q, bytes ? bytes : 16, pool, h->stream);
-    if (ee == cudaSuccess) h->mem[h->nmem++] = *q;
-    return ee;
-  };
-  void *st, *w0, *w1, *info, *doff, *dcnt, *dcount;
-  if ((e = alloc(&st, sizeof(uint32_t) * (size_t)(n_global ? n_global : 1))) != cudaSuccess ||
-      (e = alloc(&w0, sizeof(WE) * (size_t)(nl ? nl : 1))) != cudaSuccess ||
-      (e = alloc(&w1, sizeof(WE) * (size_t)(nl ? nl : 1))) != cudaSuccess ||
-      (e = alloc(&info, sizeof(DevInfo))) != cudaSuccess || (e = alloc(&doff, 64)) != cudaSuccess ||
-      (e = alloc(&dcnt, 64)) != cudaSuccess || (e = alloc(&dcount, 64)) != cudaSuccess) {
-    gc_dist_destroy(h);
-    return cuda_fail(e, "gc_dist_create: cudaMalloc");
-  }
-  // forbidden-colour planes indexed by global id (only the local bytes are ever read)
-  const int64_t pitch = (n_global + 255) / 256 * 256;
-  uint32_t np = (uint32_t)MAX_PLANES;
-  if ((uint64_t)np * (uint64_t)pitch > (16ull << 30)) {
-    const uint64_t fit = (16ull << 30) / (uint64_t)pitch;
-    np = fit < 16 ? 16u : (uint32_t)fit;
-  }
-  void *planes, *hoff, *hcur, *bnd;
-  if ((e = alloc(&planes, (size_t)pitch * np)) != cudaSuccess ||
-      (e = alloc(&bnd, (size_t)(nl ? nl : 1))) != cudaSuccess ||
-      (e = alloc(&hoff, sizeof(uint32_t) * (size_t)(n_global + 1))) != cudaSuccess ||
-      (e = alloc(&hcur, sizeof(uint32_t) * (size_t)(n_global + 1))) != cudaSuccess) {
-    gc_dist_destroy(h);
-    return cuda_fail(e, "gc_dist_create: cudaMalloc");
-  }
-  memset(&h->p, 0, sizeof(h->p));
-  Params& p = h->p;
-  p.fmp = (uint8_t*)planes;
-  p.plane = pitch;
-  p.np = np;
-  p.n = (int32_t)nl;
-  p.v_base = (int32_t)v_begin;
-  p.rp = row_ptr_local;
-  p.ci = col_idx_local;
-  p.st = st;
-  p.wl0 = (WE*)w0;
-  p.wl1 = (WE*)w1;
-  p.info = (DevInfo*)info;
-  p.max_rounds = h->max_rounds;
-  p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
-  p.t3 = o.warp_bin_max ? o.warp_bin_max : 1024;
-  p.timeout_ns = 60ull * 1000000000ull;
-  h->W[0] = (WE*)w0;
-  h->W[1] = (WE*)w1;
-  h->d_off = (uint32_t*)doff;
-  h->d_cnt = (uint32_t*)dcnt;
-  h->d_count = (unsigned long long*)dcount;
-  cudaStream_t s = h->stream;
-  // every vertex (owned or ghost) starts pending with tentative colour 1 (round 1)
-  k_fill_u32<<<h->grid, BLOCK, 0, s>>>((uint32_t*)st, n_global, 1u);
-  DK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
-  if (nl > 0) {
-    k_prologue_count<true><<<h->grid, BLOCK, 0, s>>>(p);
-    k_prologue_scatter<<<h->grid, BLOCK, 0, s>>>(p);
-  }
-  // halo adjacency: counts per remote vertex -> offsets -> lists
-  DK(cudaMemsetAsync(hoff, 0, sizeof(uint32_t) * (size_t)(n_global + 1), s));
-  if (nl > 0) k_halo_count<<<h->grid, BLOCK, 0, s>>>(p, nl, v_begin, v_end, (uint32_t*)hoff, (uint8_t*)bnd);
-  h->boundary = (uint8_t*)bnd;
-  {  // exclusive scan (CUB) of the n_global + 1 counters into hcur, then back to hoff
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (uint32_t*)hoff, (uint32_t*)hcur, (int)(n_global + 1), s);
-    void* tmp;
-    if ((e = alloc(&tmp, tmp_bytes)) != cudaSuccess) {
-      gc_dist_destroy(h);
-      return cuda_fail(e, "gc_dist_create: cudaMalloc");
-    }
-    DK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, (uint32_t*)hoff, (uint32_t*)hcur, (int)(n_global + 1), s));
-    DK(cudaMemcpyAsync(hoff, hcur, sizeof(uint32_t) * (size_t)(n_global + 1), cudaMemcpyDeviceToDevice, s));
-  }
-  uint32_t nhalo = 0;
-  DK(cudaMemcpyAsync(&nhalo, (uint32_t*)hoff + n_global, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  DK(cudaStreamSynchronize(s));
-  void* hadj;
-  if ((e = alloc(&hadj, sizeof(int32_t) * (size_t)(nhalo ? nhalo : 1))) != cudaSuccess) {
-    gc_dist_destroy(h);
-    return cuda_fail(e, "gc_dist_create: cudaMalloc");
-  }
-  DK(cudaMemcpyAsync(hcur, hoff, sizeof(uint32_t) * (size_t)(n_global + 1), cudaMemcpyDeviceToDevice, s));
-  if (nl > 0) k_halo_fill<<<h->grid, BLOCK, 0, s>>>(p, nl, v_begin, v_end, (uint32_t*)hcur, (int32_t*)hadj);
-  h->hoff = (uint32_t*)hoff;
-  h->hadj = (int32_t*)hadj;
-  DK(cudaGetLastError());
-  DevInfo hi;
-  DK(cudaMemcpyAsync(&hi, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
-  DK(cudaStreamSynchronize(s));
-  uint32_t acc = 0;
-  for (int b = 0; b < NBIN; ++b) {
-    h->off[b] = acc;
-    acc += hi.binsize[b];
-    h->cnt_in[b] = hi.binsize[b];
-  }
-  DK(cudaMemcpy(h->d_off, h->off, sizeof(h->off), cudaMemcpyHostToDevice));
+  cudaSetDevice(c->dev);
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclResult_t r = a->CommInitRank(&c->nccl, world, id, rank);
   cudaSetDevice(prev);
-  *out = h;
-  return GC_OK;
-}
-
-gc_status gc_dist_phase_a(gc_dist* h) {
-  g_err[0] = 0;
-  if (!h) return GC_ERR_INVALID_ARGUMENT;
-  if (h->round > 1 && h->p.n > 0) {
-    k_phase_a<true, false><<<h->grid, BLOCK, 0, h->stream>>>(h->p, h->round, h->W[h->cur]);
-    DK(cudaGetLastError());
+  if (r != ncclSuccess) {
+    c->nccl = nullptr;
+    gc_comm_destroy(c);
+    return nccl_fail(r, "ncclCommInitRank");
   }
-  DK(cudaStreamSynchronize(h->stream));
+  *out = c;
   return GC_OK;
 }
 
-gc_status gc_dist_phase_b(gc_dist* h, uint32_t* local_next) {
+gc_status gc_comm_init_local(gc_comm** comms_out, int32_t world, int32_t device) {
   g_err[0] = 0;
-  if (!h || !local_next) return GC_ERR_INVALID_ARGUMENT;
-  if (h->round > h->max_rounds) {
-    set_err("gc_dist_phase_b: no convergence within max_rounds=%u", h->max_rounds);
-    return GC_ERR_NO_CONVERGENCE;
-  }
-  *local_next = 0;
-  if (h->p.n > 0) {
-    launch_dist_b(h, h->grid, h->p, h->round, h->W[h->cur], h->W[h->cur ^ 1]);
-    DK(cudaGetLastError());
-    uint32_t cnt[3][NBIN];
-    DK(cudaMemcpyAsync(cnt, h->p.info->cnt, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream));
-    DK(cudaStreamSynchronize(h->stream));
-    for (int b = 0; b < NBIN; ++b) *local_next += cnt[(h->round + 1) % 3][b];
-  }
-  return GC_OK;
-}
-
-// what = 0: (v, word) of every local pending vertex of the current round (after Phase A);
-// what = 1: the local winners of the current round (after Phase B).  pairs: device buffer of
-// at least 2 * (v_end - v_begin) uint32.  *count = number of pairs written.
-gc_status gc_dist_pack(gc_dist* h, int32_t what, uint32_t* pairs, uint64_t* count) {
-  g_err[0] = 0;
-  if (!h || !count || (what != 0 && what != 1)) return GC_ERR_INVALID_ARGUMENT;
-  *count = 0;
-  if (h->p.n == 0) return GC_OK;
-  if (!pairs) return GC_ERR_INVALID_ARGUMENT;
-  DK(cudaMemcpyAsync(h->d_cnt, h->cnt_in, sizeof(h->cnt_in), cudaMemcpyHostToDevice, h->stream));
-  DK(cudaMemsetAsync(h->d_count, 0, sizeof(unsigned long long), h->stream));
-  k_pack<<<h->grid, BLOCK, 0, h->stream>>>(h->W[h->cur], h->d_off, h->d_cnt, (const uint32_t*)h->p.st, what, pairs,
-                                           h->d_count, h->boundary, h->p.v_base);
-  DK(cudaGetLastError());
-  unsigned long long c = 0;
-  DK(cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
-  DK(cudaStreamSynchronize(h->stream));
-  *count = c;
-  return GC_OK;
-}
-
-gc_status gc_dist_unpack(gc_dist* h, const uint32_t* pairs, uint64_t count) {
-  g_err[0] = 0;
-  if (!h || (count && !pairs)) return GC_ERR_INVALID_ARGUMENT;
-  if (count) {
-    k_unpack<<<h->grid, BLOCK, 0, h->stream>>>(pairs, (int64_t)count, (uint32_t*)h->p.st);
-    if (h->p.n > 0)
-      k_halo_apply<<<h->grid, BLOCK, 0, h->stream>>>(pairs, (int64_t)count, h->v_begin, h->v_end, h->hoff, h->hadj,
-                                                     h->p.fmp, h->p.plane, h->p.np);
-    DK(cudaGetLastError());
-  }
-  DK(cudaStreamSynchronize(h->stream));
-  return GC_OK;
-}
-
-// Advance to the next round (W_out becomes W_in); local_next = |W_out| from gc_dist_phase_b.
-gc_status gc_dist_next_round(gc_dist* h) {
-  g_err[0] = 0;
-  if (!h) return GC_ERR_INVALID_ARGUMENT;
-  if (h->p.n > 0) {
-    uint32_t cnt[3][NBIN];
-    DK(cudaMemcpy(cnt, h->p.info->cnt, sizeof(cnt), cudaMemcpyDeviceToHost));
-    for (int b = 0; b < NBIN; ++b) h->cnt_in[b] = cnt[(h->round + 1) % 3][b];
-  }
-  h->cur ^= 1;
-  h->round += 1;
-  return GC_OK;
-}
-
-gc_status gc_dist_finalize(gc_dist* h, uint32_t* colors_local, uint32_t* max_color_local, uint32_t* rounds) {
-  g_err[0] = 0;
-  if (!h || !max_color_local || !rounds) return GC_ERR_INVALID_ARGUMENT;
-  *max_color_local = 0;
-  *rounds = h->round;
-  if (h->p.n == 0) return GC_OK;
-  if (!colors_local || is_device_ptr(colors_local) != 1) {
-    set_err("gc_dist_finalize: colors_local must be device memory");
+  if (!comms_out || world < 1 || world > MAX_RANKS) {
+    set_err("gc_comm_init_local: world must be 1..%d", MAX_RANKS);
     return GC_ERR_INVALID_ARGUMENT;
   }
-  Params p = h->p;
-  p.colors_out = colors_local;
-  DK(cudaMemsetAsync(&h->p.info->num_colors, 0, sizeof(uint32_t), h->stream));
-  k_epilogue<<<h->grid, BLOCK, 0, h->stream>>>(p, h->round);
-  DK(cudaGetLastError());
-  DK(cudaMemcpyAsync(max_color_local, &h->p.info->num_colors, sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
-  DK(cudaStreamSynchronize(h->stream));
+  {
+    // every rank's kernel must run concurrently on its own stream: streams beyond the device's
+    // hardware connections share queues and would serialise two ranks (deadlock)
+    const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int conn = e ? atoi(e) : 8;
+    if (world > 1 && 2 * world > conn) {
+      set_err("gc_comm_init_local: %d emulated ranks need CUDA_DEVICE_MAX_CONNECTIONS >= %d (set before CUDA "
+              "initialises; it is %d)", world, 2 * world, conn);
+      return GC_ERR_UNSUPPORTED;
+    }
+  }
+  LocalGroup* g = new LocalGroup();
+  g->world = world;
+  g->slot[0].resize(world);
+  g->slot[1].resize(world);
+  for (int q = 0; q < world; ++q) comms_out[q] = nullptr;
+  for (int q = 0; q < world; ++q) {
+    gc_comm* c = new gc_comm();
+    c->rank = q;
+    c->world = world;
+    c->lg = g;
+    g->refs++;
+    gc_status s = comm_common(c, device);
+    if (s != GC_OK) {
+      gc_comm_destroy(c);
+      for (int k = 0; k < q; ++k) { gc_comm_destroy(comms_out[k]); comms_out[k] = nullptr; }
+      return s;
+    }
+    comms_out[q] = c;
+  }
   return GC_OK;
 }
 
-gc_status gc_dist_destroy(gc_dist* h) {
-  if (!h) return GC_OK;
-  for (int i = 0; i < h->nmem; ++i) cudaFreeAsync(h->mem[i], h->stream);
-  if (h->stream) {
-    cudaStreamSynchronize(h->stream);
-    cudaStreamDestroy(h->stream);
+gc_status gc_comm_destroy(gc_comm* c) {
+  if (!c) return GC_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  close_window(c);
+  if (c->boot) cudaFree(c->boot);
+  if (c->hinfo) cudaFreeHost(c->hinfo);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->nccl && nccl_api()->CommDestroy) nccl_api()->CommDestroy(c->nccl);
+  if (c->lg && --c->lg->refs == 0) delete c->lg;
+  cudaSetDevice(prev);
+  delete c;
+  return GC_OK;
+}
+
+gc_status gc_color_dist(gc_comm* c, int64_t n_global, int64_t v_begin, int64_t v_end,
+                        const int64_t* row_ptr_local, const int32_t* col_idx_local, const gc_opts* opts_in,
+                        uint32_t* colors_out_local, uint32_t* num_colors, uint32_t* rounds) {
+  g_err[0] = 0;
+  if (!c) {
+    set_err("gc_color_dist: NULL communicator");
+    return GC_ERR_INVALID_ARGUMENT;
   }
-  delete h;
+  if (num_colors) *num_colors = 0;
+  if (rounds) *rounds = 0;
+  if (c->broken) {
+    set_err("gc_color_dist: communicator unusable after an earlier failure (re-create it)");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
+  // ---- local argument checks; the verdict is agreed with the other ranks below
+  gc_status local = GC_OK;
+  gc_opts o;
+  gc_opts_default(&o);
+  Knobs kn;
+  if (opts_in) {
+    if (opts_in->struct_size != sizeof(gc_opts)) {
+      set_err("gc_color_dist: opts->struct_size=%u, expected %zu", opts_in->struct_size, sizeof(gc_opts));
+      local = GC_ERR_INVALID_ARGUMENT;
+    } else {
+      o = *opts_in;
+    }
+  }
+  const int64_t nl = v_end - v_begin;
+  if (local == GC_OK) {
+    if (!num_colors || !rounds) set_err("gc_color_dist: num_colors and rounds must not be NULL");
+    else if (o.policy > GC_POLICY_DEGREE) set_err("gc_color_dist: unknown policy %u", o.policy);
+    else if (o.flags & (GC_FLAG_PULL_FIRSTFIT | GC_FLAG_HOST_ROUNDS | GC_FLAG_VALIDATE_SYMMETRY))
+      set_err("gc_color_dist: PULL_FIRSTFIT / HOST_ROUNDS / VALIDATE_SYMMETRY are single-GPU only");
+    else if (n_global < 0 || n_global > INT32_MAX || v_begin < 0 || v_end < v_begin || v_end > n_global)
+      set_err("gc_color_dist: bad range [%lld, %lld) of n=%lld", (long long)v_begin, (long long)v_end, (long long)n_global);
+    else if (nl > 0 && (!row_ptr_local || !col_idx_local || !colors_out_local))
+      set_err("gc_color_dist: NULL row_ptr/col_idx/colors_out with a non-empty range");
+    else if ((o.flags & GC_FLAG_TRACE) && o.trace_capacity && !o.trace_worklist)
+      set_err("gc_color_dist: GC_FLAG_TRACE with NULL trace_worklist");
+    else if ((o.flags & GC_FLAG_COUNT_WORK) && !o.work)
+      set_err("gc_color_dist: GC_FLAG_COUNT_WORK with NULL work");
+    else if (!resolve_knobs(o.tuning, &kn))
+      set_err("gc_color_dist: bad opts->tuning");
+    if (g_err[0]) local = GC_ERR_INVALID_ARGUMENT;
+  }
+  Scope sc;
+  {
+    cudaError_t e = cudaGetDevice(&sc.prev_dev);
+    if (e == cudaSuccess) e = cudaSetDevice(c->dev);
+    if (e == cudaSuccess) e = get_pool(c->dev, &sc.pool);
+    if (e != cudaSuccess && local == GC_OK) local = cuda_fail(e, "gc_color_dist: device setup");
+  }
+  sc.stream = o.stream ? (cudaStream_t)o.stream : c->stream;
+  cudaStream_t s = sc.stream;
+  if (!o.stream && local == GC_OK) {  // inputs produced on the legacy default stream come first
+    cudaError_t e = after_legacy(s);
+    if (e != cudaSuccess) local = cuda_fail(e, "gc_color_dist: stream ordering");
+  }
+  // ---- agree on the arguments: same n_global / policy / flags / max_rounds, ranges tiling [0, n)
+  struct Hello {
+    int32_t status;
+    uint32_t policy, flags, max_rounds;
+    int64_t n_global, v_begin, v_end;
+  } me{(int32_t)local, o.policy, o.flags & ~(uint32_t)(GC_FLAG_TRACE | GC_FLAG_COUNT_WORK), o.max_rounds, n_global,
+       v_begin, v_end},
+      all[MAX_RANKS];
+  gc_status st = boot_allgather(c, &me, sizeof(me), all);
+  if (st != GC_OK) { c->broken = true; return st; }
+  for (int q = 0; q < c->world; ++q)
+    if (all[q].status != GC_OK) {
+      if (local == GC_OK) set_err("gc_color_dist: rank %d rejected its arguments", q);
+      return GC_ERR_INVALID_ARGUMENT;
+    }
+  for (int q = 0; q < c->world; ++q) {
+    const Hello& h = all[q];
+    const bool tiles = h.v_begin == (q == 0 ? 0 : all[q - 1].v_end) && (q + 1 < c->world || h.v_end == n_global);
+    if (h.n_global != n_global || h.policy != o.policy || h.flags != me.flags || h.max_rounds != o.max_rounds || !tiles) {
+      set_err("gc_color_dist: ranks disagree (rank %d: n=%lld [%lld, %lld) policy %u flags %u max_rounds %u); "
+              "ranges must tile [0, n) in rank order",
+              q, (long long)h.n_global, (long long)h.v_begin, (long long)h.v_end, h.policy, h.flags, h.max_rounds);
+      return GC_ERR_INVALID_ARGUMENT;
+    }
+  }
+  if (n_global == 0) return GC_OK;
+
+  // ---- window (replicas), mapped by every rank
+  const WinLayout L = win_layout(n_global);
+  if ((st = ensure_window(c, L.total)) != GC_OK) return st;
+
+  // ---- private workspace and inputs
+  // inputs
+  const bool rp_dev = nl == 0 || is_device_ptr(row_ptr_local) == 1;
+  const bool ci_dev = nl == 0 || is_device_ptr(col_idx_local) == 1;
+  const bool out_dev = nl == 0 || is_device_ptr(colors_out_local) == 1;
+  const int64_t* d_rp = row_ptr_local;
+  const int32_t* d_ci = col_idx_local;
+  int64_t m = 0;
+  void *w0 = nullptr, *w1 = nullptr, *heavy = nullptr, *dcol = colors_out_local, *dtrace = nullptr, *dinfo_bad = nullptr;
+  const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 1024;
+  const bool cw = (o.flags & GC_FLAG_COUNT_WORK) != 0;
+  const bool trace = (o.flags & GC_FLAG_TRACE) && o.trace_capacity;
+  const bool trace_dev = trace && is_device_ptr(o.trace_worklist) == 1;
+  auto prepare = [&]() -> gc_status {
+    if (nl > 0) {
+      if (!rp_dev) {
+        m = row_ptr_local[nl];
+        void* p;
+        CK(sc.alloc(&p, sizeof(int64_t) * (size_t)(nl + 1)));
+        CK(cudaMemcpyAsync(p, row_ptr_local, sizeof(int64_t) * (size_t)(nl + 1), cudaMemcpyHostToDevice, s));
+        d_rp = (const int64_t*)p;
+      } else {
+        CK(cudaMemcpyAsync(&m, d_rp + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      }
+      if (m < 0) {
+        set_err("gc_color_dist: row_ptr_local[n_local]=%lld < 0", (long long)m);
+        return GC_ERR_INVALID_GRAPH;
+      }
+      if (!ci_dev) {
+        void* p;
+        CK(sc.alloc(&p, sizeof(int32_t) * (size_t)(m ? m : 1)));
+        if (m) CK(cudaMemcpyAsync(p, col_idx_local, sizeof(int32_t) * (size_t)m, cudaMemcpyHostToDevice, s));
+        d_ci = (const int32_t*)p;
+      }
+    }
+    const int64_t nla = nl ? nl : 1;
+    const int64_t hcap = m / ((int64_t)t3 + 1) + 1;
+    CK(sc.alloc(&w0, sizeof(WE) * (size_t)nla));
+    CK(sc.alloc(&w1, sizeof(WE) * (size_t)nla));
+    CK(sc.alloc(&heavy, sizeof(WE) * (size_t)(hcap < nla ? hcap : nla)));
+    if (!out_dev) CK(sc.alloc(&dcol, sizeof(uint32_t) * (size_t)nla));
+    if (trace && !trace_dev) CK(sc.alloc(&dtrace, sizeof(uint32_t) * o.trace_capacity));
+    if (trace_dev) dtrace = o.trace_worklist;
+    if (o.flags & GC_FLAG_VALIDATE) {
+      CK(sc.alloc(&dinfo_bad, sizeof(DevInfo)));
+      CK(cudaMemsetAsync(dinfo_bad, 0, sizeof(DevInfo), s));
+      if (nl > 0) {
+        DevFacts f;
+        CK(dev_facts(c->dev, &f));
+        k_validate<<<f.sms * 8, BLOCK, 0, s>>>((int32_t)nl, v_begin, n_global, d_rp, d_ci, 0, (DevInfo*)dinfo_bad);
+        CK(cudaGetLastError());
+      }
+      unsigned long long bad = 0;
+      CK(cudaMemcpyAsync(&bad, &((DevInfo*)dinfo_bad)->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (bad) {
+        bad = ~bad;
+        set_err("gc_color_dist: invalid graph at vertex %llu: %s", bad >> 3, val_err_name((uint32_t)(bad & 7)));
+        return GC_ERR_INVALID_GRAPH;
+      }
+    }
+    return GC_OK;
+  };
+  if ((st = agree(c, prepare())) != GC_OK) return st;
+
+  // ---- kernel parameters
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.n = (int32_t)nl;
+  p.v_base = (int32_t)v_begin;
+  p.rp = d_rp;
+  p.ci = d_ci;
+  p.plane = L.pitch;
+  p.np = L.np;
+  p.fmp = c->win + L.planes;
+  p.dirty = kn.n1 ? c->win + L.dirty : nullptr;
+  p.ksplit = (int32_t*)(c->win + L.ksplit);
+  p.heavy = (WE*)heavy;
+  p.wl0 = (WE*)w0;
+  p.wl1 = (WE*)w1;
+  p.info = (DevInfo*)(c->win + L.info);
+  p.trace = (uint32_t*)dtrace;
+  p.trace_cap = trace ? o.trace_capacity : 0;
+  p.colors_out = (uint32_t*)dcol;
+  p.max_rounds = o.max_rounds ? o.max_rounds : (uint32_t)((uint64_t)n_global + 1 > 0xffffffffu ? 0xffffffffu : n_global + 1);
+  p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
+  p.t3 = t3;
+  p.dense_div = kn.dense_div ? kn.dense_div : 3;  // the dense ingest (splits, degrees) is required
+  p.dense_div_n1 = kn.dense_div_n1;
+  p.dch = kn.dch;
+  p.compact = kn.compact;
+  p.n1 = kn.n1;
+  p.n1chg = 0;       // a per-rank cost rule would make ranks mark differently: off
+  p.list_ok = 0;     // list rounds are single-GPU only
+  p.sfilter = 0;
+  p.davg2 = nl > 0 && m > 0 ? (uint32_t)((m + 2 * nl - 1) / (2 * nl)) + 1u : 1u;
+  p.timeout_ns = 60ull * 1000000000ull;
+  p.nranks = c->world;
+  p.rank = c->rank;
+  p.n_global = (int32_t)n_global;
+  p.bmask = c->win + L.bmask;
+  for (int q = 0; q <= MAX_RANKS; ++q) p.rb[q] = q < c->world ? (int32_t)all[q].v_begin : INT32_MAX;
+  Peer peers[MAX_RANKS];
+  memset(peers, 0, sizeof(peers));
+  for (int q = 0; q < c->world; ++q) {
+    uint8_t* b = c->peer[q];
+    peers[q].st = b + L.st;
+    peers[q].fmp = b + L.planes;
+    peers[q].dirty = b + L.dirty;
+    peers[q].ksplit = (int32_t*)(b + L.ksplit);
+    peers[q].info = (DevInfo*)(b + L.info);
+    peers[q].xflag = (uint32_t*)(b + L.xflag);
+  }
+  p.peer = (const Peer*)(c->win + L.peers);
+  if (kn.watchdog_ms) p.timeout_ns = (unsigned long long)kn.watchdog_ms * 1000000ull;
+  {
+    cudaError_t e = cudaMemcpyAsync(c->win + L.peers, peers, sizeof(peers), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return agree(c, cuda_fail(e, "peer table"));
+  }
+
+  // ---- launches: 8-bit state words first, wider on a (globally agreed) restart status
+  DevFacts f;
+  {
+    cudaError_t e = dev_facts(c->dev, &f);
+    if (e != cudaSuccess) return agree(c, cuda_fail(e, "dev_facts"));
+  }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct EvGuard {
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~EvGuard() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+  } evg{&ev0, &ev1};
+  int sbytes = kn.state_bytes, sbytes_used = sbytes, grid_used = 0;
+  DevInfo hinfo;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    void* fn = pick_persistent_dist(sbytes, (int)o.policy, cw, kn.variant == 1);
+    int per_sm = 0;
+    auto prepare_launch = [&]() -> gc_status {
+      // Everything that may need the context idle happens here, before the agreement below and
+      // so while no rank's kernel runs: module loading of the instance (lazy loading would
+      // load it at the first launch, and that load can wait for the other ranks' already
+      // spinning kernels: deadlock), occupancy, events; then DevInfo is zeroed.
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, fn));
+      CK(occupancy(c->dev, fn, &per_sm));
+      if (o.kernel_ms && !ev0) {
+        CK(cudaEventCreate(&ev0));
+        CK(cudaEventCreate(&ev1));
+      }
+      CK(cudaMemsetAsync(p.info, 0, sizeof(DevInfo), s));
+      CK(cudaStreamSynchronize(s));
+      return GC_OK;
+    };
+    // every rank's DevInfo is zeroed before any rank's kernel can write into it
+    if ((st = agree(c, prepare_launch())) != GC_OK) return st;
+    p.st = c->win + L.st;
+    p.epoch_base = c->epoch;
+    cudaError_t e = cudaSuccess;
+    if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
+    // one-process emulation: the ranks' kernels share this GPU and must all be resident; one CTA
+    // slot per SM is left free for the process's other work (copies, memsets, other threads)
+    int grid = c->lg ? (f.sms * (per_sm > 1 ? per_sm - 1 : 1)) / c->world : f.sms * per_sm;
+    if (grid < 1) grid = 1;
+    grid_used = grid;
+    if (ev0 && attempt == 0) cudaEventRecord(ev0, s);
+    // From the launch until this rank's kernel ends, the host thread only waits on the stream:
+    // a pageable copy here (staging-buffer setup) was observed to stall the other emulated ranks'
+    // launches behind the spinning kernels.  The read-back goes to pinned memory.
+    void* args[] = {&p};
+    e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->hinfo, p.info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) memcpy(&hinfo, c->hinfo, sizeof(DevInfo));
+    if (e != cudaSuccess) {
+      c->broken = true;  // the other ranks may be waiting in a barrier of this launch
+      return cuda_fail(e, "gc_color_dist: persistent kernel");
+    }
+    c->epoch += hinfo.bar_gen;  // every rank passed the same barriers
+    sbytes_used = sbytes;
+    if (hinfo.status == ST_NEED16 && sbytes < 2) sbytes = 2;
+    else if (hinfo.status == ST_NEED32 && sbytes < 4) sbytes = 4;
+    else break;
+  }
+  if (ev1) {
+    cudaEventRecord(ev1, s);
+    cudaEventSynchronize(ev1);
+    cudaEventElapsedTime(o.kernel_ms, ev0, ev1);
+  }
+  if (hinfo.status == ST_WATCHDOG) {
+    c->broken = true;
+    set_err("gc_color_dist: device watchdog fired (cross-rank barrier timeout; rank %d: waiting for rank %d "
+            "at epoch %u, %u of %d local CTAs arrived)", c->rank, (int)hinfo.diag[0] - 1, hinfo.diag[1], hinfo.diag[2],
+            (int)grid_used);
+    return GC_ERR_CUDA;
+  }
+  if (hinfo.status == ST_NO_CONVERGENCE) {
+    set_err("gc_color_dist: no convergence within max_rounds=%u", p.max_rounds);
+    return GC_ERR_NO_CONVERGENCE;
+  }
+  {
+    cudaError_t e = cudaSuccess;
+    if (!out_dev && nl > 0)
+      e = cudaMemcpyAsync(colors_out_local, dcol, sizeof(uint32_t) * (size_t)nl, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && trace && !trace_dev) {
+      const uint32_t k = hinfo.rounds < o.trace_capacity ? hinfo.rounds : o.trace_capacity;
+      if (k) e = cudaMemcpyAsync(o.trace_worklist, dtrace, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "gc_color_dist: outputs");
+  }
+  if (cw) {
+    memset(o.work, 0, sizeof(gc_work));
+    o.work->phase_a_vertices = hinfo.work[W_A_VERT];
+    o.work->phase_a_edges = hinfo.work[W_A_EDGE];
+    o.work->phase_b_vertices = hinfo.work[W_B_VERT];
+    o.work->phase_b_edges = hinfo.work[W_B_EDGE];
+    o.work->phase_b_gathers = hinfo.work[W_B_GATHER];
+    o.work->commit_scatter = hinfo.work[W_SCATTER];
+    o.work->pushes = hinfo.work[W_PUSH];
+    o.work->scatter_reds = hinfo.work[W_SCATTER_RED];
+    o.work->dense_a_swept = hinfo.work[W_DA_SWEEP];
+    o.work->dense_b_swept = hinfo.work[W_DB_SWEEP];
+    o.work->sparse_a_entries = hinfo.work[W_SA_ENT];
+    o.work->sparse_b_entries = hinfo.work[W_SB_ENT];
+    o.work->state_bytes = (uint64_t)sbytes_used;
+    o.work->phase_b_evaluated = hinfo.work[W_B_EVAL];
+    o.work->dense_b_evaluated = hinfo.work[W_DB_EVAL];
+    o.work->dirty_marks = hinfo.work[W_MARK];
+    o.work->tent_changes = hinfo.work[W_TCHG];
+    o.work->pending_degree_sum = hinfo.work[W_WDEG];
+  }
+  *num_colors = hinfo.num_colors;
+  *rounds = hinfo.rounds;
   return GC_OK;
 }
 

@@ -13,6 +13,7 @@
 #include "../../include/gc.h"
 #include "../../include/gc_internal.h"
 #include "sgr_kernels.cuh"
+#include "sgr_inst.h"
 
 using namespace gcdev;
 
@@ -102,11 +103,12 @@ cudaError_t occupancy(int dev, const void* fn, int* per_sm) {
 // Restores the caller's current device; frees pool allocations stream-ordered; owns an
 // internal stream when the caller passed none.
 struct Scope {
+  static constexpr int kMaxPtr = 32;
   int prev_dev = -1;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaMemPool_t pool = nullptr;
-  void* ptrs[16];
+  void* ptrs[kMaxPtr];
   int nptr = 0;
   ~Scope() {
     for (int i = 0; i < nptr; ++i) cudaFreeAsync(ptrs[i], stream);
@@ -115,6 +117,7 @@ struct Scope {
     if (prev_dev >= 0) cudaSetDevice(prev_dev);
   }
   cudaError_t alloc(void** p, size_t bytes) {
+    if (nptr >= kMaxPtr) return cudaErrorMemoryAllocation;  // bounded: never overflow ptrs[]
     if (bytes == 0) bytes = 16;
 #ifdef GC_DEFAULT_POOL
     cudaError_t e = cudaMallocAsync(p, bytes, stream);
@@ -125,6 +128,28 @@ struct Scope {
     return e;
   }
 };
+
+// A library-internal stream that starts after everything already queued on the legacy default
+// stream (where callers such as torch produce row_ptr / col_idx) without the reverse implicit
+// dependency a blocking stream would add: the stream is non-blocking and waits on an event
+// recorded on the legacy stream.  (With blocking streams, the emulated ranks of gc_dist.h
+// deadlock as soon as any thread queues work on the legacy stream: that work waits for the
+// ranks' spinning kernels, and the next rank's kernel waits for it.)
+cudaError_t after_legacy(cudaStream_t s);
+cudaError_t internal_stream(cudaStream_t* s) {
+  cudaError_t e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  return after_legacy(*s);
+}
+cudaError_t after_legacy(cudaStream_t s) {
+  cudaEvent_t ev;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(ev, cudaStreamLegacy);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev, 0);
+  cudaEventDestroy(ev);
+  return e;
+}
 
 // 1 = device (or managed) memory usable by kernels, 0 = host memory, -1 = error
 int is_device_ptr(const void* p) {
@@ -137,34 +162,20 @@ int is_device_ptr(const void* p) {
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
 }
 
-template <class S, int POL, bool PUSH, bool CW>
-void* persistent_ptr() { return (void*)sgr_persistent<S, POL, PUSH, CW>; }
-
-template <class S>
-void* pick_persistent_s(int pol, bool push, bool cw) {
-#define PK(P)                                                                                   \
-  if (pol == P) {                                                                               \
-    if (push) return cw ? persistent_ptr<S, P, true, true>() : persistent_ptr<S, P, true, false>(); \
-    return cw ? persistent_ptr<S, P, false, true>() : persistent_ptr<S, P, false, false>();     \
-  }
-  PK(HIGHER_ID) PK(LOWER_ID) PK(DEGREE)
-#undef PK
-  return nullptr;
-}
-
-template <int POL, bool CW>
-void* fat_ptr() { return (void*)sgr_persistent_fat<POL, CW>; }
-
-// state-word width: 1, 2 or 4 bytes; fat: the 3-CTA/SM variant (8-bit words, push mode)
+// The persistent kernel instances live in their own translation units (inst_*.cu, compiled
+// in parallel); each returns the host stub of the requested instance.
 void* pick_persistent(int sbytes, int pol, bool push, bool cw, bool fat = false) {
-  if (fat && sbytes == 1 && push) {
-    if (pol == HIGHER_ID) return cw ? fat_ptr<HIGHER_ID, true>() : fat_ptr<HIGHER_ID, false>();
-    if (pol == LOWER_ID) return cw ? fat_ptr<LOWER_ID, true>() : fat_ptr<LOWER_ID, false>();
-    return cw ? fat_ptr<DEGREE, true>() : fat_ptr<DEGREE, false>();
-  }
-  if (sbytes == 1) return pick_persistent_s<uint8_t>(pol, push, cw);
-  if (sbytes == 2) return pick_persistent_s<uint16_t>(pol, push, cw);
-  return pick_persistent_s<uint32_t>(pol, push, cw);
+  if (fat && sbytes == 1 && push) return gc_inst_fat(pol, cw);
+  if (sbytes == 1) return gc_inst_u8(pol, push, cw);
+  if (sbytes == 2) return gc_inst_u16(pol, push, cw);
+  return gc_inst_u32(pol, push, cw);
+}
+// multi-GPU instances (push First-Fit only), compiled with the cross-rank code
+void* pick_persistent_dist(int sbytes, int pol, bool cw, bool fat) {
+  if (fat && sbytes == 1) return gc_inst_dist_fat(pol, cw);
+  if (sbytes == 1) return gc_inst_dist_u8(pol, cw);
+  if (sbytes == 2) return gc_inst_dist_u16(pol, cw);
+  return gc_inst_dist_u32(pol, cw);
 }
 
 template <int POL, bool PUSH, bool CW>
@@ -187,6 +198,32 @@ void launch_b(int pol, bool push, bool cw, int grid, cudaStream_t s, const Param
 #undef LB
 }
 
+// Schedule knobs (include/gc.h gc_tuning), resolved to the measured defaults.
+struct Knobs {
+  int state_bytes = 1;  // first attempt's state-word width
+  uint32_t dense_div = 3, dense_div_n1 = 16, n1 = 1, list = 0, compact = 0, sfilter = 0, dch = 16, n1_chg = 0;
+  int variant = -1;
+  uint32_t watchdog_ms = 0;  // 0 = 60 s
+};
+bool resolve_knobs(const gc_tuning* t, Knobs* k) {
+  *k = Knobs();
+  if (!t) return true;
+  if (t->struct_size != sizeof(gc_tuning)) return false;
+  if (t->state_bytes == 2 || t->state_bytes == 4) k->state_bytes = t->state_bytes;
+  else if (t->state_bytes != 0 && t->state_bytes != 1) return false;
+  if (t->dense_div >= 0) k->dense_div = k->dense_div_n1 = (uint32_t)t->dense_div;
+  if (t->dense_div_n1 >= 0) k->dense_div_n1 = (uint32_t)t->dense_div_n1;
+  if (t->n1 >= 0) k->n1 = (uint32_t)t->n1;
+  if (t->list >= 0) k->list = (uint32_t)t->list;
+  if (t->compact >= 0) k->compact = (uint32_t)t->compact;
+  if (t->scatter_filter >= 0) k->sfilter = (uint32_t)t->scatter_filter;
+  if (t->dch > 0) k->dch = (uint32_t)t->dch;
+  if (t->n1_chg >= 0) k->n1_chg = (uint32_t)t->n1_chg;
+  k->variant = t->variant < 0 ? -1 : (t->variant ? 1 : 0);
+  if (t->watchdog_ms > 0) k->watchdog_ms = (uint32_t)t->watchdog_ms;
+  return true;
+}
+
 const char* val_err_name(uint32_t code) {
   switch (code) {
     case VE_ROWPTR: return "row_ptr[0] != 0 or row_ptr decreasing";
@@ -203,6 +240,15 @@ const char* val_err_name(uint32_t code) {
 extern "C" {
 
 int32_t gc_abi_version(void) { return GC_ABI_VERSION; }
+
+void gc_tuning_default(gc_tuning* t) {
+  if (!t) return;
+  memset(t, 0, sizeof(*t));
+  t->struct_size = sizeof(gc_tuning);
+  t->state_bytes = 0;
+  t->dense_div = t->dense_div_n1 = t->n1 = t->list = t->compact = t->scatter_filter = t->dch = t->n1_chg = -1;
+  t->variant = -1;
+}
 
 void gc_opts_default(gc_opts* o) {
   if (!o) return;
@@ -291,6 +337,11 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     set_err("gc_color: GC_FLAG_COUNT_WORK with NULL work");
     return GC_ERR_INVALID_ARGUMENT;
   }
+  Knobs kn;
+  if (!resolve_knobs(o.tuning, &kn)) {
+    set_err("gc_color: bad opts->tuning (struct_size or state_bytes)");
+    return GC_ERR_INVALID_ARGUMENT;
+  }
 
   Scope sc;
   CK(cudaGetDevice(&sc.prev_dev));
@@ -305,7 +356,9 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   if (o.stream) {
     sc.stream = (cudaStream_t)o.stream;
   } else {
-    CK(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+    // ordered after the legacy default stream, where the caller's producers of row_ptr /
+    // col_idx may still be running
+    CK(internal_stream(&sc.stream));
     sc.own_stream = true;
   }
   CK(get_pool(dev, &sc.pool));
@@ -345,9 +398,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   const bool cw = (o.flags & GC_FLAG_COUNT_WORK) != 0;
   void *w0, *w1, *info, *dcol = colors_out, *dtrace = nullptr;
   uint8_t* planes = nullptr;
-  // [st | plane 0 | plane 1 | ...] in one allocation so that one L2 access-policy window
-  // covers the hot per-vertex state: the state words (1, 2 or 4 bytes per vertex, placed
-  // right before plane 0 whatever their width) and the first forbidden-colour planes.
+  // [st | plane 0 | plane 1 | ...] in one allocation: the state words (1, 2 or 4 bytes per
+  // vertex, placed right before plane 0 whatever their width) and the forbidden-colour planes.
   const int64_t pitch = (n + 255) / 256 * 256;
   // up to MAX_PLANES planes (colours 1..512), at most ~16 GB of them; only the planes a run
   // reaches are ever touched (plane k from round 8k on)
@@ -360,17 +412,14 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   CK(sc.alloc(&hot, (size_t)pitch * (4 + np)));
   planes = (uint8_t*)hot + 4 * pitch;
   // dense rounds (push mode, persistent driver): per-vertex split + static heavy-vertex list
-  uint32_t dense_div = 3;  // sweep on R-MAT s24 (2, 3, 4, 6 -> 3; dirty-set graphs use dense_div_n1)
-  if (const char* dd = getenv("GC_DENSE_DIV")) dense_div = (uint32_t)atoi(dd);
+  uint32_t dense_div = kn.dense_div;  // sweep on R-MAT s24 (2, 3, 4, 6 -> 3; dirty-set graphs use dense_div_n1)
   if (!push || (o.flags & GC_FLAG_HOST_ROUNDS)) dense_div = 0;
   const uint32_t t3 = o.warp_bin_max ? o.warp_bin_max : 1024;
   void *ksplit = nullptr, *heavy = nullptr, *dirty = nullptr, *wlw0 = nullptr, *wlw1 = nullptr, *dlist = nullptr;
-  uint32_t list_ok = 0;  // list rounds (GC_LIST: 0 off (default: slower on every config
-                         // measured), 1 cost rule, 2 from round 3 on)
-  if (const char* e = getenv("GC_LIST")) list_ok = (uint32_t)atoi(e);
+  uint32_t list_ok = kn.list;  // list rounds (0 off (default: slower on every config measured),
+                               // 1 cost rule, 2 from round 3 on)
   // dirty-set rounds: needs the per-vertex splits of the dense ingest
-  uint32_t n1 = 1;
-  if (const char* e = getenv("GC_N1")) n1 = (uint32_t)atoi(e);
+  uint32_t n1 = kn.n1;
   if (!dense_div) n1 = 0;
   if (dense_div) {
     if (m < 0) {
@@ -402,7 +451,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   // ---- optional validation (C9): one warp per vertex
   if (o.flags & (GC_FLAG_VALIDATE | GC_FLAG_VALIDATE_SYMMETRY)) {
     const int vgrid = prop.sms * 8;
-    k_validate<<<vgrid, BLOCK, 0, s>>>((int32_t)n, d_rp, d_ci, (o.flags & GC_FLAG_VALIDATE_SYMMETRY) ? 1 : 0,
+    k_validate<<<vgrid, BLOCK, 0, s>>>((int32_t)n, 0, n, d_rp, d_ci, (o.flags & GC_FLAG_VALIDATE_SYMMETRY) ? 1 : 0,
                                        (DevInfo*)info);
     CK(cudaGetLastError());
     unsigned long long bad = 0;
@@ -424,10 +473,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.fmp = push ? planes : nullptr;
   p.plane = pitch;
   p.np = np;
-  {
-    const char* f = getenv("GC_SCATTER_FILTER");
-    p.sfilter = (f && f[0] == '1') ? 1u : 0u;
-  }
+  p.sfilter = kn.sfilter;
   p.wl0 = (WE*)w0;
   p.wl1 = (WE*)w1;
   p.info = (DevInfo*)info;
@@ -444,13 +490,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.t1 = o.thread_bin_max ? o.thread_bin_max : 16;
   p.t3 = t3;   // sweep on R-MAT s24: 128/256/512/768/1024/1536/2048 -> 1024 best
   p.dense_div = dense_div;
-  if (const char* c = getenv("GC_COMPACT")) p.compact = (uint32_t)atoi(c);
-  p.dch = 16;  // sweep 2..32 on the three configs: 16 (R-MAT s24 -1 %)
-  if (const char* c = getenv("GC_DCH")) p.dch = (uint32_t)atoi(c) ? (uint32_t)atoi(c) : 16u;
-  if (const char* c = getenv("GC_N1_CHG")) p.n1chg = (uint32_t)atoi(c);
-  p.dense_div_n1 = 16;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16
-  if (const char* dd = getenv("GC_DENSE_DIV_N1")) p.dense_div_n1 = (uint32_t)atoi(dd);
-  if (const char* dd = getenv("GC_DENSE_DIV")) p.dense_div_n1 = (uint32_t)atoi(dd);  // one knob for tests
+  p.compact = kn.compact;
+  p.dch = kn.dch;            // sweep 2..32 on the three configs: 16 (R-MAT s24 -1 %)
+  p.n1chg = kn.n1_chg;
+  p.dense_div_n1 = kn.dense_div_n1;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16
   p.ksplit = (int32_t*)ksplit;
   p.dirty = (uint8_t*)dirty;
   p.wlw0 = (int32_t*)wlw0;
@@ -461,7 +504,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.davg2 = n > 0 && m > 0 ? (uint32_t)((m + 2 * n - 1) / (2 * n)) + 1u : 1u;  // successors + 1
   p.n1gain = n > 0 ? (uint32_t)(m / (2 * n) < 8 ? m / (2 * n) : 8) : 0u;
   p.heavy = (WE*)heavy;
-  p.timeout_ns = 60ull * 1000000000ull;
+  p.timeout_ns = kn.watchdog_ms ? (unsigned long long)kn.watchdog_ms * 1000000ull : 60ull * 1000000000ull;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (o.kernel_ms) {
@@ -473,57 +516,6 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     cudaEvent_t a, b;
     ~EvGuard() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
   } evg{ev0, ev1};
-  // L2 residency of the hot per-vertex state: an access-policy window marks [st | planes] as
-  // persisting (the streamed CSR and worklists are "streaming" misses), within a temporary
-  // persisting set-aside.  Stream attribute, limit and persisting lines are restored or reset
-  // before returning.  GC_L2_PERSIST=0 disables it (ablation).
-  struct L2Window {
-    cudaStream_t s = nullptr;
-    bool on = false;
-    size_t prev = 0;
-    ~L2Window() {
-      if (!on) return;
-      cudaStreamAttrValue av;
-      memset(&av, 0, sizeof(av));
-      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
-      cudaCtxResetPersistingL2Cache();
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev);
-    }
-  } l2w;
-  const char* l2env = getenv("GC_L2_PERSIST");
-  const bool want_window = !(l2env && l2env[0] == '0');
-  auto set_window = [&](int sbytes) -> cudaError_t {
-    if (!want_window) return cudaSuccess;
-    int maxp = 0, maxw = 0;
-    cudaError_t e;
-    if ((e = cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev)) != cudaSuccess) return e;
-    if (maxp <= 0 || maxw <= 0) return cudaSuccess;
-    // the state words plus as many forbidden-colour planes as the set-aside holds
-    // (GC_L2_PLANES caps the plane count; tuning)
-    const size_t sb = (size_t)pitch * sbytes;
-    if (sb > (size_t)maxp + (size_t)maxp / 2) return cudaSuccess;
-    uint32_t kp = 0;
-    while (kp < np && sb + (size_t)pitch * (kp + 1) <= (size_t)maxp) ++kp;
-    if (const char* lp = getenv("GC_L2_PLANES")) kp = kp < (uint32_t)atoi(lp) ? kp : (uint32_t)atoi(lp);
-    size_t bytes = sb + (size_t)pitch * kp;
-    if (bytes > (size_t)maxw) bytes = (size_t)maxw;
-    const size_t limit = bytes < (size_t)maxp ? bytes : (size_t)maxp;
-    if (!l2w.on) {
-      if ((e = cudaDeviceGetLimit(&l2w.prev, cudaLimitPersistingL2CacheSize)) != cudaSuccess) return e;
-      l2w.s = s;
-      l2w.on = true;
-    }
-    if ((e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit)) != cudaSuccess) return e;
-    cudaStreamAttrValue av;
-    memset(&av, 0, sizeof(av));
-    av.accessPolicyWindow.base_ptr = (uint8_t*)planes - sb;
-    av.accessPolicyWindow.num_bytes = bytes;
-    av.accessPolicyWindow.hitRatio = (float)((double)limit / (double)bytes);
-    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    return cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
-  };
   int sbytes = 4, sbytes_used = 4;
   if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
     // ---- persistent cooperative kernel: the whole run in one launch
@@ -536,7 +528,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     // run is then repeated with the wider words (at most two restarts).
     // kernel variant: bounded degree (<= 64) and >= 8 entries per row -> 3 CTAs/SM (sgr_kernels.cuh)
     bool fat = false;
-    if (push && n1 && m >= 8 * n) {
+    if (kn.variant < 0 && push && n1 && m >= 8 * n) {
       void* dmax;
       CK(sc.alloc(&dmax, sizeof(uint32_t)));
       CK(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
@@ -547,15 +539,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       CK(cudaStreamSynchronize(s));
       fat = mx <= 64;
     }
-    if (const char* f = getenv("GC_FAT")) fat = f[0] == '1';
-    sbytes = 1;
-    if (const char* sw = getenv("GC_STATE_BYTES")) {  // diagnostics: force a width
-      const int f = atoi(sw);
-      if (f == 1 || f == 2 || f == 4) sbytes = f;
-    }
+    if (kn.variant >= 0) fat = kn.variant == 1;
+    sbytes = kn.state_bytes;
     for (int attempt = 0; attempt < 3; ++attempt) {
       p.st = (uint8_t*)planes - (int64_t)sbytes * pitch;
-      CK(set_window(sbytes));
       void* fn = pick_persistent(sbytes, (int)o.policy, push, cw, fat);
       int per_sm = 0;
       CK(occupancy(dev, fn, &per_sm));
@@ -579,7 +566,6 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   } else {
     // ---- host-driven rounds (ablation): one launch per phase, |W| read every round
     p.st = (uint8_t*)planes - 4 * pitch;
-    CK(set_window(4));
     const int grid = prop.sms * 4;
     if (push) k_prologue_count<true><<<grid, BLOCK, 0, s>>>(p);
     else k_prologue_count<false><<<grid, BLOCK, 0, s>>>(p);
@@ -712,7 +698,7 @@ gc_status gc_verify(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, c
   CK(cudaGetDevice(&sc.prev_dev));
   const int dev = device >= 0 ? device : sc.prev_dev;
   CK(cudaSetDevice(dev));
-  CK(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+  CK(internal_stream(&sc.stream));  // ordered after the legacy default stream
   sc.own_stream = true;
   CK(get_pool(dev, &sc.pool));
   cudaStream_t s = sc.stream;

@@ -41,7 +41,21 @@
 
 #include <stdint.h>
 
+// The multi-GPU kernel instances (inst_dist_*.cu) are compiled from the same source with
+// GC_DIST_TU defined: their symbols live in namespace gcdev_dist and kDist switches the
+// cross-rank code on.  Everywhere else kDist is false and that code is compiled out, so the
+// single-GPU kernels carry none of it (registers, stack).
+#ifdef GC_DIST_TU
+#define gcdev gcdev_dist
+#endif
+
 namespace gcdev {
+
+#ifdef GC_DIST_TU
+constexpr bool kDist = true;
+#else
+constexpr bool kDist = false;
+#endif
 
 constexpr int NBIN = 2;            // 0 = thread probe + warp continuation, 1 = CTA per vertex
 #ifndef GC_PROBE
@@ -90,7 +104,9 @@ struct DevInfo {
   unsigned long long work[W_N];
   unsigned long long bad;       // validation / verify: ~(smallest offending key), 0 = none
   uint32_t err_code;
-  uint32_t pad2[31];
+  uint32_t gtot[3];             // multi-GPU: global |W| by round (r % 3), summed by the ranks' barrier leaders
+  uint32_t diag[4];             // watchdog diagnostics: [0] 1 + rank not heard from, [1] epoch, [2] arrivals seen
+  uint32_t pad2[24];
   uint32_t bar_count;           // grid barrier (own 128-B lines)
   uint32_t pad3[31];
   uint32_t bar_gen;
@@ -106,9 +122,24 @@ struct __align__(16) WE {
   long long beg;
 };
 
+// Multi-GPU: every rank holds full-size (global-indexed) replicas of
+// the per-vertex arrays that other ranks read or write; a rank's kernel reaches the other
+// ranks' replicas through these peer pointers (CUDA-IPC mappings over NVLink, or plain
+// device pointers when the ranks are emulated on one GPU).
+constexpr int MAX_RANKS = 8;
+struct Peer {
+  void* st;                     // state words (ghost copies of the rank's boundary vertices)
+  uint8_t* fmp;                 // forbidden-colour planes (REDs of cut-edge commits)
+  uint8_t* dirty;               // dirty marks (successors across the cut)
+  int32_t* ksplit;              // DEGREE: degrees of boundary vertices
+  DevInfo* info;                // status, global |W|, max degree, num_colors
+  uint32_t* xflag;              // cross-rank barrier flags: [MAX_RANKS][32], slot q written by rank q
+};
+
 struct Params {
   int32_t n;                    // rows held here (all vertices, or one partition's range)
-  int32_t v_base;               // global id of local row 0 (0 on one GPU); st is global-indexed
+  int32_t v_base;               // global id of local row 0 (0 on one GPU); per-vertex arrays
+                                //   (st, fmp, dirty, ksplit) are global-indexed
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;
   void* st;                     // state word per vertex (uint8_t, uint16_t or uint32_t)
@@ -143,7 +174,31 @@ struct Params {
   uint32_t t1;                  // winners of degree <= t1 scatter by themselves, larger: warp-wide
   uint32_t t3;                  // degree <= t3: bin 0 (thread + warp); above: bin 1 (one CTA)
   unsigned long long timeout_ns;
+  // ---- multi-GPU (nranks > 1); on one GPU nranks = 1 and none of this is read
+  int32_t nranks, rank;
+  int32_t n_global;
+  uint32_t epoch_base;          // cross-rank barrier epochs already used by earlier launches
+  int32_t rb[MAX_RANKS + 1];    // rank q owns [rb[q], rb[q+1]); entries past nranks = INT32_MAX
+  uint8_t* bmask;               // global-indexed: bit q set when rank q holds local vertex v as a ghost
+  const Peer* peer;             // [nranks] in device memory (indexed by rank at run time; a table in
+                                //   the kernel parameters would be copied to the stack)
 };
+
+__device__ __forceinline__ bool dist(const Params& p) { return kDist && p.nranks > 1; }
+// Rank owning global vertex w (ranges are contiguous and ordered by rank).
+__device__ __forceinline__ int owner(const Params& p, int32_t w) {
+  int q = 0;
+#pragma unroll
+  for (int k = 1; k < MAX_RANKS; ++k) q += w >= p.rb[k];
+  return q;
+}
+// Base of the forbidden-colour planes / dirty marks holding vertex w (its owner's).
+__device__ __forceinline__ uint8_t* fmp_of(const Params& p, int32_t w) {
+  return dist(p) ? p.peer[owner(p, w)].fmp : p.fmp;
+}
+__device__ __forceinline__ uint8_t* dirty_of(const Params& p, int32_t w) {
+  return dist(p) ? p.peer[owner(p, w)].dirty : p.dirty;
+}
 
 struct Work {
   unsigned long long v[W_N];
@@ -263,6 +318,14 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -274,6 +337,30 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// ---------------------------------------------------------------- multi-GPU propagation
+// Run status (restart / no convergence / watchdog): every rank must stop at the same barrier,
+// so a status is written into every rank's DevInfo before the barrier that reads it.
+__device__ __forceinline__ void set_status(const Params& p, uint32_t s) {
+  atomicExch(&p.info->status, s);
+  if (dist(p))
+    for (int q = 0; q < p.nranks; ++q)
+      if (q != p.rank) atomicExch(&p.peer[q].info->status, s);
+}
+// A local vertex's new state word goes to the replicas of the ranks that hold it as a ghost
+// (the owners of its neighbours): the device-initiated exchange of SURVEY N2.
+template <class S>
+__device__ __forceinline__ void bcast_word(const Params& p, int32_t v, uint32_t word, uint32_t m) {
+  while (m) {
+    const int q = __ffs(m) - 1;
+    m &= m - 1;
+    sts((S*)p.peer[q].st + v, word);
+  }
+}
+template <class S>
+__device__ __forceinline__ void bcast_word(const Params& p, int32_t v, uint32_t word) {
+  if (dist(p)) bcast_word<S>(p, v, word, lds(p.bmask + v));
+}
+
 // ---------------------------------------------------------------- grid barrier
 // Generation barrier over all co-resident CTAs of the cooperative launch.  The arriving
 // CTA publishes its phase with a fence + relaxed atomic; waiters spin on RELAXED loads (an
@@ -283,14 +370,48 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Returns false when the run must stop.  Deliberately NOT inlined: with the barrier inlined
 // into the round loop, ptxas 12.9 was observed to reuse a live uniform register (holding a
 // worklist base pointer) as scratch for the barrier address (truncated-pointer faults).
-__device__ __noinline__ bool grid_sync(const Params& p) {
+//
+// Multi-GPU: the barrier spans every rank's grid.  Each CTA fences at system scope (its
+// stores/REDs into peer replicas are then ordered before its arrival); the last CTA of a rank
+// to arrive adds the rank's |W_{r+1}| into every rank's global count (nxt >= 0), then
+// release-stores the epoch into its slot of every rank's flag array and acquire-polls its own
+// flags until every rank has signalled the epoch, and only then flips the local generation.
+// Epochs continue across launches (p.epoch_base), so the flags are never reset.
+static __device__ __noinline__ void xrank_sync(const Params& p, uint32_t gen, int nxt) {
+  if (nxt >= 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int b = 0; b < NBIN; ++b) t += ld_relaxed(&p.info->cnt[nxt][b]);
+    for (int q = 0; q < p.nranks; ++q) atomicAdd(&p.peer[q].info->gtot[nxt], t);
+  }
+  __threadfence_system();
+  const uint32_t ep = p.epoch_base + gen;
+  for (int q = 0; q < p.nranks; ++q) st_release_sys(p.peer[q].xflag + 32 * p.rank, ep);
+  const unsigned long long t0 = globaltimer();
+  const uint32_t* mine = p.peer[p.rank].xflag;
+  for (int q = 0; q < p.nranks; ++q) {
+    while ((int32_t)(ld_acquire_sys(mine + 32 * q) - ep) < 0) {
+      __nanosleep(32);
+      if (globaltimer() - t0 > p.timeout_ns) {
+        p.info->diag[0] = 1u + (uint32_t)q;
+        p.info->diag[1] = ep;
+        atomicExch(&p.info->status, (uint32_t)ST_WATCHDOG);
+        return;
+      }
+    }
+  }
+}
+
+static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
   __syncthreads();
   if (threadIdx.x == 0) {
     DevInfo* I = p.info;
     const uint32_t gen = ld_relaxed(&I->bar_gen);
-    __threadfence();
+    if (dist(p)) __threadfence_system();
+    else __threadfence();
     const uint32_t arrived = atomicAdd(&I->bar_count, 1u);
     if (arrived == gridDim.x - 1) {
+      if (dist(p)) xrank_sync(p, gen + 1, nxt);
       atomicExch(&I->bar_count, 0u);
       st_release(&I->bar_gen, gen + 1);
     } else {
@@ -298,6 +419,7 @@ __device__ __noinline__ bool grid_sync(const Params& p) {
       while (ld_relaxed(&I->bar_gen) == gen) {
         __nanosleep(64);
         if (globaltimer() - t0 > p.timeout_ns) {
+          I->diag[2] = ld_relaxed(&I->bar_count);
           atomicExch(&I->status, (uint32_t)ST_WATCHDOG);
           break;
         }
@@ -571,9 +693,21 @@ template <class S>
 __device__ __forceinline__ void red_plane(uint8_t* pl, int32_t w, uint32_t bit) {
   red_or((uint32_t*)(pl + (w & ~3)), bit << ((w & 3) * 8));
 }
+// Multi-GPU: the plane byte of a remote neighbour lives in its owner's planes (peer RED).
+template <class S>
+__device__ __forceinline__ void red_color(const Params& p, int64_t off, int32_t w, uint32_t bit) {
+  red_plane<S>((dist(p) ? fmp_of(p, w) : p.fmp) + off, w, bit);
+}
 template <class S, int STEP, bool CW>
 __device__ __forceinline__ void scatter(const Params& p, uint32_t color, int64_t start, int64_t end, Work& wk) {
   if (color > 8u * p.np) return;
+  if (dist(p)) {
+    const int64_t off = (int64_t)((color - 1) >> 3) * p.plane;
+    const uint32_t bit = 1u << ((color - 1) & 7);
+    for (int64_t e = start; e < end; e += STEP) red_color<S>(p, off, ldc(p.ci, e), bit);
+    if (CW) wk.v[W_SCATTER_RED] += (unsigned long long)(end > start ? (end - start + STEP - 1) / STEP : 0);
+    return;
+  }
   uint8_t* const pl = p.fmp + (int64_t)((color - 1) >> 3) * p.plane;
   const uint32_t bit = 1u << ((color - 1) & 7);
   const S* st = (const S*)p.st;

@@ -49,13 +49,16 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       b = bin_of(p, deg);
       sts(st + p.v_base + v, 1u);
       if (PUSH) sts(p.fmp + p.v_base + v, 0u);  // planes are indexed by global id
-      if (p.dirty) sts(p.dirty + v, 0u);
+      if (p.dirty) sts(p.dirty + e.v, 0u);
       e.k = 0;
       if (dense && POL != DEGREE) {
         e.k = b == 0 ? split_fast(p, e.v, e.beg, end) : row_split(p, e.v, e.beg, end);
-        p.ksplit[v] = e.k;
+        p.ksplit[e.v] = e.k;
       } else if (dense) {
-        p.ksplit[v] = (int32_t)deg;  // DEGREE: the array holds the degrees (one load per compare)
+        p.ksplit[e.v] = (int32_t)deg;  // DEGREE: the array holds the degrees (one load per compare)
+        if (dist(p)) {  // ... and the ranks holding v as a ghost need its degree
+          for (uint32_t m = lds(p.bmask + e.v); m; m &= m - 1) p.peer[__ffs(m) - 1].ksplit[e.v] = (int32_t)deg;
+        }
       }
     }
 #pragma unroll
@@ -74,15 +77,45 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       }
     }
   }
-  if (wide) atomicExch(&p.info->status, (uint32_t)ST_NEED32);
+  if (wide) set_status(p, ST_NEED32);
   maxdeg = __reduce_max_sync(FULL, maxdeg);
-  if (lane == 0 && maxdeg) atomicMax(&p.info->maxdeg, maxdeg);
+  if (lane == 0 && maxdeg) {  // multi-GPU: the global max (decides the dirty-set rounds everywhere)
+    if (dist(p)) for (int q = 0; q < p.nranks; ++q) atomicMax(&p.peer[q].info->maxdeg, maxdeg);
+    else atomicMax(&p.info->maxdeg, maxdeg);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.info->wlp[0] = (unsigned long long)p.wl0;
     p.info->wlp[1] = (unsigned long long)p.wl1;
   }
   __syncthreads();
   if (threadIdx.x < NBIN && s_cnt[threadIdx.x]) atomicAdd(&p.info->binsize[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// Multi-GPU pre-pass (before the ingest): every replica word starts pending with tentative
+// colour 1 (round 1), and bmask[v] of every local vertex v = the set of other ranks owning a
+// neighbour of v — exactly the ranks that read v's state word (the graph is symmetric), so the
+// only ones its tentative colours and commit are sent to.  One warp per local vertex.
+__device__ __forceinline__ void prologue_dist(const Params& p) {
+  const int64_t T = (int64_t)gridDim.x * BLOCK;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = T >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < p.n; u += nw) {
+    const int64_t beg = ldr(p.rp, u), end = ldr(p.rp, u + 1);
+    uint32_t m = 0;
+    for (int64_t e = beg + lane; e < end; e += 32) {
+      const int32_t w = ldc(p.ci, e);
+      if (w < p.v_base || w >= p.v_base + p.n) m |= 1u << owner(p, w);
+    }
+    m = __reduce_or_sync(FULL, m);
+    if (lane == 0) sts(p.bmask + p.v_base + u, m);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.info->gtot[1] = (uint32_t)p.n_global;
+}
+template <class S>
+__device__ __forceinline__ void fill_replica(const Params& p) {
+  S* st = (S*)p.st;
+  for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < p.n_global; v += (int64_t)gridDim.x * BLOCK)
+    sts(st + v, 1u);
 }
 
 // P1: W_1 = V, split into bin segments of wl0 (warp-aggregated cursors; order within a
@@ -186,8 +219,12 @@ __device__ __forceinline__ BSmem& bsmem() {
 // (ST_NEED16).
 template <class S>
 __device__ __forceinline__ void store_tent(const Params& p, S* st, int32_t v, uint32_t t) {
-  if (sizeof(S) == 1 && t > SW<S>::CMASK) atomicExch(&p.info->status, (uint32_t)ST_NEED16);
-  else sts(st + v, t);
+  if (sizeof(S) == 1 && t > SW<S>::CMASK) {
+    set_status(p, ST_NEED16);
+  } else {
+    sts(st + v, t);
+    bcast_word<S>(p, v, t);
+  }
 }
 
 // First free colour from the planes, 0 when all np planes are full.
@@ -223,7 +260,7 @@ __device__ __forceinline__ void mark_dirty(const Params& p, int32_t v, int64_t b
     for (int u = 0; u < 4; ++u) w[u] = e + u < hi ? ldc(p.ci, e + u) : -1;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (w[u] >= 0) sts(p.dirty + w[u], 1u);
+      if (w[u] >= 0) sts(dirty_of(p, w[u]) + w[u], 1u);
   }
   if (CW) wk.v[W_MARK] += (unsigned long long)(hi - lo + 1);
 }
@@ -354,6 +391,8 @@ __device__ __forceinline__ void reset_next(const Params& p, uint32_t r) {
     p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
     if (threadIdx.x == 0) {
+      // multi-GPU: the other ranks add into this copy only at the end of Phase B of round r
+      p.info->gtot[(r + 1) % 3] = 0;
       p.info->chg[(r + 1) % 3] = 0;
       p.info->wl_cnt[(r + 1) % 3] = 0;
       p.info->dl_cnt[(r + 1) % 3] = 0;
@@ -408,13 +447,15 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
   zero_plane(p, r);
   const int lane = threadIdx.x & 31;
   const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
-  const int64_t ngroups = ((int64_t)p.n + 15) / 16;
+  // groups of 16 global ids aligned to 16 covering this rank's range [vlo, vend)
+  const int64_t vlo = p.v_base, vend = (int64_t)p.v_base + p.n, lo16 = vlo & ~(int64_t)15;
+  const int64_t ngroups = (vend - lo16 + 15) / 16;
   const int64_t g0 = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31);
   uint32_t nchg = 0;
   int32_t* clist = bsmem().clist[threadIdx.x >> 5];
   for (int64_t gb = g0; gb < ngroups; gb += nthreads) {
     const int64_t g = gb + lane;
-    const int64_t v0 = g * 16;
+    const int64_t v0 = lo16 + g * 16;
     uint32_t fb = 0, chgm = 0;
     if (g < ngroups) {
       constexpr int NW = 4 * (int)sizeof(S);          // 32-bit words holding 16 state words
@@ -440,7 +481,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
       for (int h = 0; h < 16; ++h) {
         const int wi = h / PER, sh = (h % PER) * 8 * (int)sizeof(S);
         const uint32_t sv = (w[wi] >> sh) & SMASK;
-        if (v0 + h < p.n && !(sv & SW<S>::COMMIT)) {
+        if (v0 + h >= vlo && v0 + h < vend && !(sv & SW<S>::COMMIT)) {
           const uint32_t b0 = (pw[h >> 2] >> ((h & 3) * 8)) & 0xffu;
           const uint32_t b1 = (pw1[h >> 2] >> ((h & 3) * 8)) & 0xffu;
           const uint32_t t = b0 != 0xffu   ? (uint32_t)__ffs(b0 ^ 0xffu)
@@ -449,7 +490,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           if (t == 0) {
             fb |= 1u << h;
           } else if (t != (sv & SW<S>::CMASK)) {
-            if (sizeof(S) == 1 && t > SW<S>::CMASK) atomicExch(&p.info->status, (uint32_t)ST_NEED16);
+            if (sizeof(S) == 1 && t > SW<S>::CMASK) set_status(p, ST_NEED16);
             w[wi] = (w[wi] & ~(SMASK << sh)) | ((t & SMASK) << sh);
             dirty = true;
             chgm |= 1u << h;
@@ -457,17 +498,35 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
         }
       }
       if (dirty) {
+        if (dist(p) && (v0 < vlo || v0 + 16 > vend)) {
+          // a group straddling a rank boundary also holds ghost words that their owner may be
+          // writing into this replica right now: store only this rank's changed words
 #pragma unroll
-        for (int i = 0; i < (int)sizeof(S); ++i)
-          stv(st + v0 + i * (16 / sizeof(S)), make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+          for (int h = 0; h < 16; ++h)
+            if (chgm >> h & 1u) sts(st + v0 + h, (w[h / PER] >> ((h % PER) * 8 * (int)sizeof(S))) & SMASK);
+        } else {
+#pragma unroll
+          for (int i = 0; i < (int)sizeof(S); ++i)
+            stv(st + v0 + i * (16 / sizeof(S)), make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+        }
+        if (dist(p)) {  // changed boundary vertices: the new tentative colour to their ghosts
+          const uint4 bq = ldv(p.bmask + v0);
+          const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+          for (int h = 0; h < 16; ++h) {
+            const uint32_t bm = (bw[h >> 2] >> ((h & 3) * 8)) & 0xffu;
+            if ((chgm >> h & 1u) && bm)
+              bcast_word<S>(p, (int32_t)(v0 + h), (w[h / PER] >> ((h % PER) * 8 * (int)sizeof(S))) & SMASK, bm);
+          }
+        }
       }
       nchg += __popc(chgm);
       if (CW) {  // sum of the degrees of the pending vertices (SURVEY §8(d) units)
 #pragma unroll
         for (int h = 0; h < 16; ++h) {
           const int wi = h / PER, sh = (h % PER) * 8 * (int)sizeof(S);
-          if (v0 + h < p.n && !(((w[wi] >> sh) & SMASK) & SW<S>::COMMIT))
-            wk.v[W_WDEG] += (unsigned long long)(ldr(p.rp, v0 + h + 1) - ldr(p.rp, v0 + h));
+          if (v0 + h >= vlo && v0 + h < vend && !(((w[wi] >> sh) & SMASK) & SW<S>::COMMIT))
+            wk.v[W_WDEG] += (unsigned long long)(RP(p, v0 + h + 1) - RP(p, v0 + h));
         }
       }
     }
@@ -485,7 +544,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
         int64_t lo = 0, hi = 0;
         if (i0 + lane < tot) {
           const int32_t v = clist[i0 + lane];
-          const int64_t beg = ldr(p.rp, v), end = ldr(p.rp, v + 1);
+          const int64_t beg = RP(p, v), end = RP(p, v + 1);
           const int32_t k = POL != DEGREE ? ldks(p.ksplit + v) : 0;
           lo = POL == HIGHER_ID ? beg + k : beg;
           hi = POL == LOWER_ID ? beg + k : end;
@@ -508,7 +567,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (w[u] >= 0) sts(p.dirty + w[u], 1u);
+            if (w[u] >= 0) sts(dirty_of(p, w[u]) + w[u], 1u);
         }
       }
       __syncwarp();
@@ -648,7 +707,10 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
   }
   // winners commit; the forbidden masks of their neighbours get their colour bit
   const bool win = state == 2;
-  if (win) sts(st + e.v, tent | SW<S>::COMMIT);
+  if (win) {
+    sts(st + e.v, tent | SW<S>::COMMIT);
+    bcast_word<S>(p, e.v, tent | SW<S>::COMMIT);
+  }
   if (rec_round) rec_winners(p, rec_round, win, e.v, lane);
   if (PUSH) {
     const bool sc = win && tent <= 8u * p.np;
@@ -669,9 +731,9 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
         const int64_t bo = __shfl_sync(FULL, e.beg, oc);
         const uint32_t to = __shfl_sync(FULL, tent, oc);
-        pl[u] = p.fmp + (int64_t)((to - 1) >> 3) * p.plane;
         wb[u] = 1u << ((to - 1) & 7);
         w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
+        pl[u] = (dist(p) && w[u] >= 0 ? fmp_of(p, w[u]) : p.fmp) + (int64_t)((to - 1) >> 3) * p.plane;
       }
       if (p.sfilter) {
         uint32_t sw[4];
@@ -755,6 +817,7 @@ __device__ __forceinline__ bool cta_vertex(const Params& p, WE& e, uint32_t tent
   if (!lose) {
     if (threadIdx.x == 0) {
       sts(st + e.v, tent | SW<S>::COMMIT);
+      bcast_word<S>(p, e.v, tent | SW<S>::COMMIT);
       if (rec_round)
         (((rec_round & 1) ? p.wlw1 : p.wlw0))[atomicAdd(&p.info->wl_cnt[rec_round % 3], 1u)] = e.v;
     }
@@ -865,6 +928,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
   constexpr uint32_t CM = SW<S>::CMASK;
   constexpr int DIR = POL == HIGHER_ID ? -1 : 1;
   const uint32_t v0 = base + lane * VPL;
+  const uint32_t vlo = (uint32_t)p.v_base;  // ids below it (first batch of a rank): not ours
   // level 1: state words, row offsets, splits of the lane's VPL vertices (independent loads)
   uint32_t states = 0;  // 8 bits per slot: 0 inactive, 1 lose, 2 win, 3 undecided
   {
@@ -872,19 +936,20 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     int64_t rpv[VPL + 1];
     int32_t kv[VPL];
 #pragma unroll
-    for (int h = 0; h < VPL; ++h) sw[h] = v0 + h < cend ? lds(st + v0 + h) : SW<S>::COMMIT;
+    for (int h = 0; h < VPL; ++h) sw[h] = v0 + h >= vlo && v0 + h < cend ? lds(st + v0 + h) : SW<S>::COMMIT;
 #pragma unroll
-    for (int h = 0; h <= VPL; ++h) rpv[h] = v0 + h <= cend ? ldr(p.rp, (int64_t)v0 + h) : 0;
+    for (int h = 0; h <= VPL; ++h) rpv[h] = v0 + h >= vlo && v0 + h <= cend ? RP(p, (int64_t)v0 + h) : 0;
 #pragma unroll
-    for (int h = 0; h < VPL; ++h) kv[h] = (POL != DEGREE && v0 + h < cend) ? ldks(p.ksplit + v0 + h) : 0;
+    for (int h = 0; h < VPL; ++h)
+      kv[h] = (POL != DEGREE && v0 + h >= vlo && v0 + h < cend) ? ldks(p.ksplit + v0 + h) : 0;
     uint32_t dv[VPL];
 #pragma unroll
-    for (int h = 0; h < VPL; ++h) dv[h] = mark && v0 + h < cend ? lds(p.dirty + v0 + h) : 1u;
+    for (int h = 0; h < VPL; ++h) dv[h] = mark && v0 + h >= vlo && v0 + h < cend ? lds(p.dirty + v0 + h) : 1u;
 #pragma unroll
     for (int h = 0; h < VPL; ++h) {
       const int sl = lane * VPL + h;
       const int64_t beg = rpv[h], deg = rpv[h + 1] - rpv[h];
-      const bool pend = v0 + h < cend && !(sw[h] & SW<S>::COMMIT) && deg <= (int64_t)p.t3;
+      const bool pend = v0 + h >= vlo && v0 + h < cend && !(sw[h] & SW<S>::COMMIT) && deg <= (int64_t)p.t3;
       const bool act = pend && dv[h];
       if (mark && pend) {
         if (dv[h]) sts(p.dirty + v0 + h, 0u);
@@ -1020,7 +1085,10 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
   // commit: winners set the top bit of their own state word
 #pragma unroll
   for (int h = 0; h < VPL; ++h)
-    if (((states >> (8 * h)) & 0xffu) == 2u) sts(st + v0 + h, sg.tent[lane * VPL + h] | SW<S>::COMMIT);
+    if (((states >> (8 * h)) & 0xffu) == 2u) {
+      sts(st + v0 + h, sg.tent[lane * VPL + h] | SW<S>::COMMIT);
+      bcast_word<S>(p, (int32_t)(v0 + h), sg.tent[lane * VPL + h] | SW<S>::COMMIT);
+    }
   if (rec_round) {
 #pragma unroll
     for (int h = 0; h < VPL; ++h) rec_winners(p, rec_round, ((states >> (8 * h)) & 0xffu) == 2u, (int32_t)(v0 + h), lane);
@@ -1059,7 +1127,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       for (int u = 0; u < 4; ++u) {
         if (w[u] < 0 || (skip >> u & 1u)) continue;
         const uint32_t t = sg.tent[own[u]];
-        red_plane<S>(p.fmp + (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
+        red_color<S>(p, (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
         if (CW && p.sfilter) wk.v[W_SCATTER_RED] += 1;
       }
     }
@@ -1305,7 +1373,9 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     }
   }
   const uint32_t nwarps = gridDim.x * WARPS;
-  const uint32_t nv = (uint32_t)p.n;
+  // chunk offsets c count from lo16 (this rank's first id rounded down to 16): vertex lo16 + c
+  const uint32_t vlo = (uint32_t)p.v_base, vend = vlo + (uint32_t)p.n, lo16 = vlo & ~15u;
+  const uint32_t nv = vend - lo16;
   uint32_t* q = &p.info->qctr[cur][0][0];
   uint32_t lost_cnt = 0;
   if ((mark || p.compact) && !push_out) {
@@ -1316,9 +1386,9 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     int* s_first = sm.cwfirst[warp];
     constexpr uint32_t CHD = 512;
     for (uint32_t c0 = pop_chunk(q, CHD, lane); c0 < nv; c0 = pop_chunk(q, CHD, lane)) {
-      const uint32_t v0 = c0 + 16u * lane;
+      const uint32_t v0 = lo16 + c0 + 16u * lane;
       uint32_t cand = 0, pend = 0;
-      if (v0 < nv) {
+      if (v0 < vend) {
         const uint4 dq = mark ? ldv(p.dirty + v0) : make_uint4(0, 0, 0, 0);
         const uint32_t dw[4] = {dq.x, dq.y, dq.z, dq.w};
         uint32_t sw[4 * sizeof(S)];
@@ -1334,7 +1404,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
         for (int h = 0; h < 16; ++h) {
           constexpr int PER = 4 / (int)sizeof(S);
           const uint32_t sv = sw[h / PER] >> ((h % PER) * 8 * (int)sizeof(S));
-          const bool pd = v0 + h < nv && !(sv & SW<S>::COMMIT);
+          const bool pd = v0 + h >= vlo && v0 + h < vend && !(sv & SW<S>::COMMIT);
           pend |= (uint32_t)pd << h;
           cand |= (uint32_t)(pd && (!mark || ((dw[h >> 2] >> ((h & 3) * 8)) & 0xffu))) << h;
         }
@@ -1357,8 +1427,8 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
         if (act) {
           e.v = clist[i0 + lane];
           tent = lds(st + e.v) & SW<S>::CMASK;
-          e.beg = ldr(p.rp, e.v);
-          end = ldr(p.rp, e.v + 1);
+          e.beg = RP(p, e.v);
+          end = RP(p, e.v + 1);
           if (POL != DEGREE) e.k = ldks(p.ksplit + e.v);
           act = end - e.beg <= (int64_t)p.t3;  // heavy vertices (and their marks): the CTA loop
           if (act && mark) sts(p.dirty + e.v, 0u);
@@ -1373,7 +1443,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       if (bins.size[1]) {
         for (uint32_t m = pend; m; m &= m - 1) {
           const int32_t v = (int32_t)(v0 + __ffs(m) - 1);
-          if (ldr(p.rp, v + 1) - ldr(p.rp, v) > (int64_t)p.t3) ++heavy_pend;
+          if (RP(p, v + 1) - RP(p, v) > (int64_t)p.t3) ++heavy_pend;
         }
       }
       const uint32_t np = __reduce_add_sync(FULL, (uint32_t)__popc(pend) - heavy_pend);
@@ -1384,8 +1454,8 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   }
   const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (p.dch * nwarps)) / WB * WB));
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nv; c0 = pop_chunk(q, ch, lane)) {
-    const uint32_t cend = min(c0 + ch, (uint32_t)p.n);
-    for (uint32_t bse = c0; bse < cend; bse += WB)
+    const uint32_t cend = lo16 + min(c0 + ch, nv);
+    for (uint32_t bse = lo16 + c0; bse < cend; bse += WB)
       batch_b_wide<S, POL, PUSH, CW>(p, lane, bse, cend, sm.seg[warp], push_out, mark, pu, lost_cnt, wk, rec_round,
                                      r == 1);
   }
@@ -1414,7 +1484,10 @@ __device__ __forceinline__ void epilogue(const Params& p) {
     mx = c > mx ? c : mx;
   }
   mx = __reduce_max_sync(FULL, mx);
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(&p.info->num_colors, mx);
+  if ((threadIdx.x & 31) == 0 && mx) {
+    if (dist(p)) for (int q = 0; q < p.nranks; ++q) atomicMax(&p.peer[q].info->num_colors, mx);
+    else atomicMax(&p.info->num_colors, mx);
+  }
 }
 
 template <bool CW>
@@ -1440,6 +1513,11 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   Work wk;
   wk.zero();
   const bool dense0 = PUSH && p.dense_div != 0;
+  if (dist(p)) {  // multi-GPU: replica fill + ghost masks (one cross-rank barrier)
+    fill_replica<S>(p);
+    prologue_dist(p);
+    if (!grid_sync(p)) return;
+  }
   prologue_count<S, POL, PUSH>(p, dense0);
   if (!grid_sync(p)) return;
   Bins bins;
@@ -1497,10 +1575,14 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
     } else {
       phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, mark, wk, list_next);
     }
-    if (!grid_sync(p)) return;
+    // multi-GPU: |W_r| of the trace is the global one (the phase wrote the local count)
+    if (dist(p) && blockIdx.x == 0 && threadIdx.x == 0 && p.trace && r <= p.trace_cap)
+      p.trace[r - 1] = ld_relaxed(&p.info->gtot[cur]);
+    if (!grid_sync(p, dist(p) ? (int)((r + 1) % 3) : -1)) return;
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
     uint32_t left;
     if (list) left = (uint32_t)tot - ld_relaxed(&p.info->wl_cnt[cur]);
+    else if (dist(p)) left = ld_relaxed(&p.info->gtot[(r + 1) % 3]);  // global: every rank stops together
     else left = next_total(p, r);
     if (list_next) {
       list = true;
@@ -1508,7 +1590,7 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
     }
     if (left == 0) break;
     if (r >= p.max_rounds) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&p.info->status, (uint32_t)ST_NO_CONVERGENCE);
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&p.info->status, (uint32_t)ST_NO_CONVERGENCE);  // same r on every rank
       flush_work<CW>(p, wk);
       return;
     }
@@ -1517,6 +1599,7 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   epilogue<S>(p);
   flush_work<CW>(p, wk);
   if (blockIdx.x == 0 && threadIdx.x == 0) p.info->rounds = r;
+  if (dist(p)) grid_sync(p);  // every rank's num_colors holds the global max before the host reads it
 }
 
 template <class S, int POL, bool PUSH, bool CW>
@@ -1531,6 +1614,7 @@ __global__ void __launch_bounds__(BLOCK, 3) sgr_persistent_fat(Params p) {
   sgr_body<uint8_t, POL, true, CW>(p);
 }
 
+#ifndef GC_INST_TU  // the non-template kernels below live in gc_api.cu only
 // Max degree (host-side kernel selection).
 __global__ void __launch_bounds__(BLOCK) k_maxdeg(int32_t n, const int64_t* __restrict__ rp, uint32_t* out) {
   uint32_t mx = 0;
@@ -1593,18 +1677,22 @@ __device__ __forceinline__ void report_bad(DevInfo* I, int64_t v, uint32_t code)
   atomicMax(&I->bad, ~key);
 }
 
-__global__ void __launch_bounds__(BLOCK) k_validate(int32_t n, const int64_t* __restrict__ rp,
-                                                    const int32_t* __restrict__ ci, int symmetry, DevInfo* I) {
+// Rows [v_base, v_base + n) of a graph on n_global vertices (one GPU: v_base = 0, n_global = n);
+// the symmetry check needs every row, so it is single-GPU only.
+__global__ void __launch_bounds__(BLOCK) k_validate(int32_t n, int64_t v_base, int64_t n_global,
+                                                    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                    int symmetry, DevInfo* I) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * BLOCK) >> 5;
-  if (gw == 0 && lane == 0 && __ldg(rp) != 0) report_bad(I, 0, VE_ROWPTR);
-  for (int64_t v = gw; v < n; v += nw) {
-    const int64_t beg = __ldg(rp + v), end = __ldg(rp + v + 1);
+  if (gw == 0 && lane == 0 && __ldg(rp) != 0) report_bad(I, v_base, VE_ROWPTR);
+  for (int64_t u = gw; u < n; u += nw) {
+    const int64_t v = v_base + u;
+    const int64_t beg = __ldg(rp + u), end = __ldg(rp + u + 1);
     if (end < beg) { if (lane == 0) report_bad(I, v, VE_ROWPTR); continue; }
     for (int64_t e = beg + lane; e < end; e += 32) {
       const int32_t w = __ldg(ci + e);
-      if (w < 0 || w >= n) { report_bad(I, v, VE_RANGE); continue; }
+      if (w < 0 || w >= n_global) { report_bad(I, v, VE_RANGE); continue; }
       if (w == v) report_bad(I, v, VE_SELF);
       if (e > beg && __ldg(ci + e - 1) >= w) report_bad(I, v, VE_ORDER);
       if (symmetry) {
@@ -1656,5 +1744,7 @@ __global__ void __launch_bounds__(BLOCK) k_verify(int32_t n, const int64_t* __re
     if (bad && lane == 0) report_bad(I, v, 2);
   }
 }
+
+#endif  // GC_INST_TU
 
 }  // namespace gcdev

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _declared_symbols():
-    src = open(os.path.join(ROOT, "include", "gc.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("gc.h", "gc_dist.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(gc_[a-z_]+)\s*\(", src)))
 
@@ -22,7 +22,9 @@ def _declared_symbols():
 def test_header_declares_the_north_star_call():
     syms = _declared_symbols()
     for s in ("gc_color", "gc_verify", "gc_opts_default", "gc_status_string",
-              "gc_last_error_message", "gc_partition_edge_balanced", "gc_abi_version"):
+              "gc_last_error_message", "gc_partition_edge_balanced", "gc_abi_version",
+              "gc_tuning_default", "gc_comm_init", "gc_color_dist", "gc_comm_destroy",
+              "gc_comm_init_local", "gc_nccl_unique_id"):
         assert s in syms
 
 
@@ -45,7 +47,11 @@ def test_opts_layout_and_defaults():
     o = gc.default_opts()
     assert o.struct_size == ctypes.sizeof(gc.Opts) == 96
     assert o.policy == 0 and o.flags == gc.FLAG_VALIDATE and o.device == -1
-    assert gc.abi_version() == 1
+    assert gc.abi_version() == 2
+    t = gc.make_tuning(dict(n1=2))
+    assert t.struct_size == 64 and t.n1 == 2 and t.dense_div == -1 and t.variant == -1
+    with pytest.raises(ValueError):
+        gc.make_tuning(dict(bogus=1))
     assert gc.status_string(2) == "GC_ERR_INVALID_GRAPH"
 
 

@@ -1,14 +1,20 @@
-"""Multi-GPU path (include/gc_dist.h, paper_1606_06025_b200/dist.py).
+"""Multi-GPU path: include/gc_dist.h (gc_comm_init / gc_color_dist / gc_comm_destroy) and its
+binding paper_1606_06025_b200/dist.py.
 
-CPU (gloo, world_size 2): the round driver and its two per-round all-gathers run over a real
-torch.distributed gloo group; each rank's partition kernels are replaced by a numpy test
-double with the kernels' per-phase semantics (FakePartition), so the host logic — partition
-bounds, local CSR slices, packing, all-gather of variable-size pair lists, termination by
-global |W| — is exercised exactly as on GPUs.  The gathered colouring must equal the oracle.
+CPU (no GPU; gloo world_size 2 where processes are involved): the host logic around the
+library — NCCL unique-id broadcast over torch.distributed, edge-balanced bounds, local CSR
+slices in global ids, assembling the ranks' colour ranges — and the library's argument checks
+that run before any CUDA call.  The gloo test colours each rank's range with the CPU oracle
+restricted to that range (test infrastructure), so the gathered result must equal the oracle.
 
-GPU: the real kernels, P partitions inside one process (exchange = in-process), must give
-the single-GPU colouring bit for bit for P = 1..8 (partition invariance).
+GPU: the real device-initiated kernels on the single test GPU through the
+one-process emulation (gc_comm_init_local: `world` ranks, one host thread each, every rank's
+persistent kernel resident side by side, peer stores into sibling windows, cross-rank
+barriers): colours, num_colors, rounds and |W_r| trace must equal the oracle's for every
+cover of [0, n) — edge-balanced, random, with empty ranges — every policy and every schedule
+knob (partition invariance).
 """
+import ctypes
 import os
 import socket
 
@@ -18,72 +24,7 @@ import pytest
 import oracle
 import workloads as wl
 
-COMMIT = 0x80000000
-CMASK = 0x7FFFFFFF
-
-
-class FakePartition:
-    """numpy model of one gc_dist partition (test double for the CUDA kernels)."""
-
-    def __init__(self, n_global, v_begin, v_end, rp_local, ci_local, policy="higher_id"):
-        import torch
-        self.torch = torch
-        self.n, self.vb, self.ve = n_global, v_begin, v_end
-        self.rp, self.ci = np.asarray(rp_local), np.asarray(ci_local)
-        self.policy = policy
-        self.st = np.ones(n_global, dtype=np.uint32)        # everyone pending with tent 1
-        self.W = list(range(v_begin, v_end))
-        self.Wn = []
-        self.round = 1
-
-    def adj(self, v):
-        i = v - self.vb
-        return self.ci[self.rp[i]:self.rp[i + 1]]
-
-    def recolors(self, v, w):
-        return v > w if self.policy == "higher_id" else v < w
-
-    def phase_a(self):
-        if self.round == 1:
-            return
-        for v in self.W:
-            used = {int(self.st[w] & CMASK) for w in self.adj(v) if self.st[w] & COMMIT}
-            c = 1
-            while c in used:
-                c += 1
-            self.st[v] = c
-
-    def phase_b(self):
-        lose = []
-        for v in self.W:
-            t = self.st[v] & CMASK
-            if any((self.st[w] & CMASK) == t and self.recolors(v, int(w)) for w in self.adj(v)):
-                lose.append(v)
-        ls = set(lose)
-        for v in self.W:
-            if v not in ls:
-                self.st[v] |= COMMIT
-        self.Wn = lose
-        return len(lose)
-
-    def pack(self, what):
-        vs = [v for v in self.W if what == 0 or (self.st[v] & COMMIT)]
-        out = np.zeros(2 * len(vs), dtype=np.uint32)
-        out[0::2] = vs
-        out[1::2] = self.st[vs] if vs else []
-        return self.torch.from_numpy(out.view(np.int32).copy())
-
-    def unpack(self, pairs):
-        a = pairs.cpu().numpy().view(np.uint32)
-        self.st[a[0::2]] = a[1::2]
-
-    def next_round(self):
-        self.W, self.Wn = self.Wn, []
-        self.round += 1
-
-    def finalize(self):
-        c = self.st[self.vb:self.ve] & CMASK
-        return self.torch.from_numpy(c.astype(np.int32)), int(c.max()) if len(c) else 0, self.round
+POLICIES = ["higher_id", "lower_id", "degree"]
 
 
 def _free_port():
@@ -94,90 +35,253 @@ def _free_port():
     return p
 
 
-GRAPHS = {"rmat": lambda: wl.rmat(10, 8, seed=3), "mesh": lambda: wl.mesh2d(24, 17, 0.3, seed=2),
-          "k9": lambda: wl.complete(9), "path": lambda: wl.path(33)}
+def random_bounds(n, parts, seed):
+    """A cover of [0, n) by `parts` contiguous ranges (some possibly empty)."""
+    rng = np.random.default_rng(seed)
+    cuts = np.sort(rng.integers(0, n + 1, parts - 1))
+    return np.concatenate([[0], cuts, [n]]).astype(np.int64)
 
 
-def _worker(rank, world, port, name, policy, q):
-    import torch
-    import torch.distributed as dist
-    from paper_1606_06025_b200.dist import TorchComm, local_slice, run_rounds
+# ---------------------------------------------------------------- CPU: host logic
+
+def test_local_slice_and_assemble():
     from paper_1606_06025_b200 import partition_edge_balanced
+    from paper_1606_06025_b200.dist import assemble, local_slice
+    g = wl.rmat(9, 8)
+    for bounds in (partition_edge_balanced(g.row_ptr, 3), random_bounds(g.n, 5, 1),
+                   np.array([0, 0, g.n, g.n], np.int64)):
+        rebuilt, parts = [], []
+        for k in range(len(bounds) - 1):
+            b, e = int(bounds[k]), int(bounds[k + 1])
+            rpl, cil = local_slice(g.row_ptr, g.col_idx, b, e)
+            assert rpl[0] == 0 and rpl[-1] == len(cil)
+            rebuilt.append(cil)
+            parts.append(np.arange(b, e, dtype=np.uint32))
+        assert np.array_equal(np.concatenate(rebuilt), g.col_idx)
+        assert np.array_equal(assemble(parts, bounds), np.arange(g.n, dtype=np.uint32))
+
+
+def test_dist_argument_checks_without_gpu():
+    import paper_1606_06025_b200 as gc
+    import paper_1606_06025_b200.dist  # noqa: F401  (declares the argtypes)
+    lib = gc._lib
+    nc, rd = ctypes.c_uint32(5), ctypes.c_uint32(5)
+    assert lib.gc_color_dist(None, 10, 0, 10, None, None, None, None, ctypes.byref(nc), ctypes.byref(rd)) == 1
+    hs = (ctypes.c_void_p * 9)()
+    assert lib.gc_comm_init_local(hs, 0, 0) == 1
+    assert lib.gc_comm_init_local(hs, 9, 0) == 1
+    h = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.gc_comm_init(ctypes.byref(h), 2, 2, uid, 0) == 1      # rank >= world
+    assert lib.gc_comm_init(ctypes.byref(h), 0, 9, uid, 0) == 1      # world > GC_MAX_RANKS
+    assert lib.gc_comm_destroy(None) == 0
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_1606_06025_b200 import partition_edge_balanced
+    from paper_1606_06025_b200.dist import broadcast_uid, local_slice
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        g = GRAPHS[name]()
+        uid = broadcast_uid(lambda: bytes(range(128)))        # rank 0's id reaches every rank
+        g = wl.rmat(10, 8, seed=3)
         bounds = partition_edge_balanced(g.row_ptr, world)
         b, e = int(bounds[rank]), int(bounds[rank + 1])
         rpl, cil = local_slice(g.row_ptr, g.col_idx, b, e)
-        part = FakePartition(g.n, b, e, rpl, cil, policy)
-        res = run_rounds([part], TorchComm())
-        q.put((rank, b, e, res.colors_local[0].numpy().tolist(), res.num_colors, res.rounds, res.exchanged_pairs))
+        # stand-in for this rank's gc_color_dist output: the oracle's colours of the range
+        mine = oracle.sgr(g)[0][b:e]
+        parts = [None] * world
+        dist.all_gather_object(parts, (b, e, mine.tolist(), int(rpl[-1]), len(cil)))
+        q.put((rank, uid, parts, bounds.tolist()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", sorted(GRAPHS))
-@pytest.mark.parametrize("policy", ["higher_id", "lower_id"])
-def test_gloo_world2_matches_oracle(name, policy):
+def test_gloo_world2_uid_broadcast_and_gather():
     import torch.multiprocessing as mp
+    from paper_1606_06025_b200.dist import assemble
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, policy, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=120) for _ in procs]
+    outs = sorted(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    outs.sort()
-    g = GRAPHS[name]()
-    colors = np.zeros(g.n, dtype=np.uint32)
-    for rank, b, e, c, nc, r, sent in outs:
-        colors[b:e] = c
-    ref, nc_ref, r_ref = oracle.sgr(g, policy)
-    assert np.array_equal(colors, ref)
-    assert all(o[4] == nc_ref and o[5] == r_ref for o in outs)
-    assert sum(o[6] for o in outs) > 0
+    g = wl.rmat(10, 8, seed=3)
+    for rank, uid, parts, bounds in outs:
+        assert uid == bytes(range(128))
+        assert [(b, e) for b, e, *_ in parts] == list(zip(bounds[:-1], bounds[1:]))
+        assert all(nnz == ncol for *_, nnz, ncol in parts)
+        colors = assemble([np.array(c, np.uint32) for _, _, c, _, _ in parts], bounds)
+        assert np.array_equal(colors, oracle.sgr(g)[0])
 
 
-def test_local_slice_and_bounds():
-    from paper_1606_06025_b200.dist import local_slice
-    from paper_1606_06025_b200 import partition_edge_balanced
-    g = wl.rmat(9, 8)
-    b = partition_edge_balanced(g.row_ptr, 3)
-    rebuilt = []
-    for k in range(3):
-        rpl, cil = local_slice(g.row_ptr, g.col_idx, int(b[k]), int(b[k + 1]))
-        assert rpl[0] == 0 and rpl[-1] == len(cil)
-        rebuilt.append(cil)
-    assert np.array_equal(np.concatenate(rebuilt), g.col_idx)
+# ---------------------------------------------------------------- GPU: the real kernels
+
+@pytest.fixture(scope="module")
+def gcd():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1606_06025_b200 as gc
+    import paper_1606_06025_b200.dist as d
+    return gc, d
+
+
+def _dev(g):
+    import torch
+    return (torch.from_numpy(np.ascontiguousarray(g.row_ptr)).cuda(),
+            torch.from_numpy(np.ascontiguousarray(g.col_idx) if g.m else np.zeros(1, np.int32)).cuda())
+
+
+def _check_dist(d, g, bounds, policy, **kw):
+    # a lost rank fails the test in seconds (the barriers of these small graphs take microseconds)
+    kw["tuning"] = dict(kw.get("tuning") or {}, watchdog_ms=20000)
+    rp, ci = _dev(g)
+    colors, results = d.color_partitioned_local(rp, ci, bounds, policy, trace=True, **kw)
+    ref, nc, r, tr = oracle.sgr(g, policy, trace=True)
+    if not np.array_equal(colors, ref):
+        bad = np.nonzero(colors != ref)[0]
+        raise AssertionError(f"{g.name} {policy} bounds={list(bounds)} {kw}: {len(bad)} mismatches, "
+                             f"first v={bad[0]} gpu={colors[bad[0]]} oracle={ref[bad[0]]}")
+    for res in results:
+        assert res.num_colors == nc and res.rounds == r, (res.num_colors, nc, res.rounds, r)
+        assert res.trace == tr
+    return results
+
+
+DIST_GRAPHS = [
+    lambda: wl.rmat(13, 8, seed=4), lambda: wl.mesh2d(64, 48, 0.3), lambda: wl.complete(40),
+    lambda: wl.star(300, center_last=True), lambda: wl.stencil27(9, 7, 5), lambda: wl.rmat(12, 16, wl.GRAPH500, 3),
+    lambda: wl.disjoint_union(wl.rmat(10, 8), wl.star(3000, center_last=True), wl.path(77)),
+]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("policy", ["higher_id", "lower_id"])
-def test_gpu_partition_invariance(parts, policy):
-    """P partitions on one GPU == single-GPU gc_color == oracle, bit for bit."""
-    import torch
-    import paper_1606_06025_b200 as gc
-    from paper_1606_06025_b200.dist import color_partitioned
-    for g in (wl.rmat(13, 8, seed=4), wl.mesh2d(64, 48, 0.3), wl.complete(40), wl.star(300, center_last=True)):
-        rp = torch.from_numpy(g.row_ptr).cuda()
-        ci = torch.from_numpy(g.col_idx if g.m else np.zeros(1, np.int32)).cuda()
-        colors, nc, rounds = color_partitioned(rp, ci, parts, policy)
-        one = gc.color(rp, ci, policy=policy)
-        ref, nc_ref, r_ref = oracle.sgr(g, policy)
-        assert torch.equal(colors.cpu(), one.colors.cpu())
-        assert np.array_equal(colors.cpu().numpy().view(np.uint32), ref)
-        assert nc == nc_ref == one.num_colors and rounds == r_ref == one.rounds
+@pytest.mark.parametrize("policy", POLICIES)
+def test_gpu_dist_edge_balanced(gcd, parts, policy):
+    """Edge-balanced ranges, every policy: bit-identical to the oracle (and so to one GPU)."""
+    gc, d = gcd
+    for make in DIST_GRAPHS:
+        g = make()
+        _check_dist(d, g, gc.partition_edge_balanced(g.row_ptr, parts), policy)
 
 
 @pytest.mark.gpu
-def test_gpu_dist_degree_policy_unsupported():
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_dist_random_covers(gcd, seed):
+    """Arbitrary covers, including empty and unaligned ranges (dense sweeps straddling ranks)."""
+    gc, d = gcd
+    for make in DIST_GRAPHS[:5]:
+        g = make()
+        parts = [2, 3, 5, 8, 4, 7][seed]
+        b = random_bounds(g.n, parts, seed)
+        for policy in POLICIES:
+            _check_dist(d, g, b, policy)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tuning", [dict(n1=0), dict(n1=2), dict(n1=2, dense_div=1), dict(dense_div=1000000000),
+                                    dict(dense_div=1), dict(state_bytes=2), dict(state_bytes=4),
+                                    dict(n1=2, state_bytes=2), dict(compact=1), dict(variant=1)],
+                         ids=lambda t: ",".join(f"{k}={v}" for k, v in t.items()))
+def test_gpu_dist_schedules(gcd, tuning):
+    """Every schedule knob (dense/sparse switch, dirty-set rounds with remote marks, state width,
+    kernel variant) leaves the multi-rank colouring unchanged."""
+    gc, d = gcd
+    for make in (DIST_GRAPHS[0], DIST_GRAPHS[1], DIST_GRAPHS[4], lambda: wl.complete(70)):
+        g = make()
+        for policy in POLICIES:
+            _check_dist(d, g, gc.partition_edge_balanced(g.row_ptr, 3), policy, tuning=tuning)
+            _check_dist(d, g, random_bounds(g.n, 4, 11), policy, tuning=tuning)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [127, 128, 130])
+def test_gpu_dist_state_restart(gcd, k):
+    """Colours > 127: every rank stops at the same barrier and restarts with 16-bit words."""
+    gc, d = gcd
+    g = wl.complete(k)
+    res = _check_dist(d, g, np.array([0, 5, 64, k], np.int64), "higher_id")
+    assert res[0].num_colors == k
+
+
+@pytest.mark.gpu
+def test_gpu_dist_matches_one_gpu_rmat16(gcd):
+    """BASELINE configs[0] (R-MAT s16) on 2/4/8 emulated ranks == gc_color == oracle."""
     import torch
-    import paper_1606_06025_b200 as gc
-    from paper_1606_06025_b200.dist import color_partitioned
-    g = wl.path(10)
-    with pytest.raises(gc.GcError):
-        color_partitioned(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda(), 2, "degree")
+    gc, d = gcd
+    g = wl.config_graph("rmat16")
+    rp, ci = _dev(g)
+    one = gc.color(rp, ci)
+    for parts in (2, 4, 8):
+        colors, res = d.color_partitioned_local(rp, ci, gc.partition_edge_balanced(g.row_ptr, parts))
+        assert np.array_equal(colors, one.colors.cpu().numpy().view(np.uint32))
+        assert res[0].rounds == one.rounds and res[0].num_colors == one.num_colors
+    assert torch.cuda.is_available()
+
+
+@pytest.mark.gpu
+def test_gpu_dist_comm_reuse_and_host_buffers(gcd):
+    """One communicator across calls and graph sizes (window grows, epochs continue); host
+    (numpy) inputs and outputs."""
+    gc, d = gcd
+    comms = d.local_group(3)
+    try:
+        for g in (wl.rmat(11, 8), wl.rmat(13, 8, seed=2), wl.path(50), wl.rmat(11, 8)):
+            b = gc.partition_edge_balanced(g.row_ptr, 3)
+            rp, ci = _dev(g)
+            colors, _ = d.color_partitioned_local(rp, ci, b, comms=comms)
+            assert np.array_equal(colors, oracle.sgr(g)[0])
+            colors_h, _ = d.color_partitioned_local(g.row_ptr, g.col_idx, b, comms=comms)
+            assert np.array_equal(colors_h, oracle.sgr(g)[0])
+    finally:
+        for c in comms:
+            c.close()
+
+
+@pytest.mark.gpu
+def test_gpu_dist_disagreement_and_errors(gcd):
+    """Ranges that do not tile [0, n), or a rank whose rows are invalid: every rank returns the
+    error (none is left waiting), and the communicator stays usable."""
+    import threading
+    gc, d = gcd
+    g = wl.rmat(10, 8)
+    rp, ci = _dev(g)
+    comms = d.local_group(2)
+    try:
+        errs = [None, None]
+
+        def run(q, b, e, cil):
+            rpl, _ = d.local_slice(rp, ci, b, e)
+            try:
+                d.color_dist(comms[q], g.n, b, e, rpl.contiguous(), cil)
+            except gc.GcError as ex:
+                errs[q] = ex.status
+        # gap between the ranges
+        th = [threading.Thread(target=run, args=(0, 0, 100, ci[:int(g.row_ptr[100])].contiguous())),
+              threading.Thread(target=run, args=(1, 101, g.n, ci[int(g.row_ptr[101]):].contiguous()))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert errs == [1, 1]
+        # rank 1's rows hold an out-of-range id: GC_ERR_INVALID_GRAPH reported everywhere
+        errs = [None, None]
+        bad = ci[int(g.row_ptr[512]):].clone()
+        bad[0] = g.n + 5
+        th = [threading.Thread(target=run, args=(0, 0, 512, ci[:int(g.row_ptr[512])].contiguous())),
+              threading.Thread(target=run, args=(1, 512, g.n, bad))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert errs == [2, 2]
+        colors, _ = d.color_partitioned_local(rp, ci, [0, 512, g.n], comms=comms)
+        assert np.array_equal(colors, oracle.sgr(g)[0])
+    finally:
+        for c in comms:
+            c.close()

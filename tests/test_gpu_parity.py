@@ -85,47 +85,53 @@ def test_parity_variants(gc, kw):
             _check(gc, g, pol, **kw)
 
 
-@pytest.mark.parametrize("env", [dict(GC_STATE_BYTES="2"), dict(GC_STATE_BYTES="4"),
-                                 dict(GC_SCATTER_FILTER="1"), dict(GC_L2_PERSIST="0"),
-                                 dict(GC_DENSE_DIV="0"), dict(GC_DENSE_DIV="1"),
-                                 dict(GC_DENSE_DIV="1000000000"), dict(GC_N1="0"), dict(GC_N1="2"),
-                                 dict(GC_N1="2", GC_DENSE_DIV="1"), dict(GC_N1="2", GC_DENSE_DIV="1000000000"),
-                                 dict(GC_N1="2", GC_STATE_BYTES="2"), dict(GC_LIST="0"), dict(GC_LIST="2"),
-                                 dict(GC_LIST="2", GC_N1="2"), dict(GC_LIST="2", GC_DENSE_DIV="1"),
-                                 dict(GC_COMPACT="1"), dict(GC_COMPACT="1", GC_N1="0"), dict(GC_FAT="1"),
-                                 dict(GC_FAT="1", GC_N1="2", GC_DENSE_DIV="1"), dict(GC_FAT="0")],
-                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
-def test_parity_env_variants(gc, env, monkeypatch):
-    """Forced state-word widths, filtered commit scatter, no L2 window: same result."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+TUNINGS = [dict(state_bytes=2), dict(state_bytes=4), dict(scatter_filter=1),
+           dict(dense_div=0), dict(dense_div=1), dict(dense_div=1000000000), dict(n1=0), dict(n1=2),
+           dict(n1=2, dense_div=1), dict(n1=2, dense_div=1000000000), dict(n1=2, state_bytes=2),
+           dict(list=0), dict(list=2), dict(list=2, n1=2), dict(list=2, dense_div=1), dict(compact=1),
+           dict(compact=1, n1=0), dict(variant=1), dict(variant=1, n1=2, dense_div=1), dict(variant=0),
+           dict(dch=2), dict(n1_chg=4), dict(dense_div=4, dense_div_n1=64)]
+
+
+def _tid(t):
+    return ",".join(f"{k}={v}" for k, v in t.items())
+
+
+@pytest.mark.parametrize("tuning", TUNINGS, ids=_tid)
+def test_parity_tuning_variants(gc, tuning):
+    """Every schedule knob of gc_tuning (forced state widths, dense/sparse switch, dirty-set
+    and list rounds, filtered commit scatter, kernel variant): same result."""
     for g in (wl.rmat(13, 8, seed=7), wl.rmat(11, 16, wl.GRAPH500, 5), wl.complete(70), wl.complete(130),
               wl.disjoint_union(wl.star(3000), wl.mesh2d(40, 30, 0.3), wl.star(2000, center_last=True)),
               wl.stencil27(9, 7, 5)):
         for pol in POLICIES:
-            _check(gc, g, pol)
-            _check(gc, g, pol, warp_bin_max=8)
-        _check(gc, g, "higher_id", host_rounds=True)
+            _check(gc, g, pol, tuning=tuning)
+            _check(gc, g, pol, warp_bin_max=8, tuning=tuning)
+        _check(gc, g, "higher_id", host_rounds=True, tuning=tuning)
 
 
-@pytest.mark.parametrize("env", [dict(GC_LIST="2"), dict(GC_LIST="2", GC_N1="2"), dict(GC_LIST="2", GC_DENSE_DIV="1"),
-                                 dict(GC_LIST="2", GC_DENSE_DIV="0"), dict(GC_LIST="1")],
-                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
-def test_parity_list_rounds(gc, env, monkeypatch):
+@pytest.mark.parametrize("tuning", [dict(list=2), dict(list=2, n1=2), dict(list=2, dense_div=1),
+                                    dict(list=2, dense_div=0), dict(list=1)], ids=_tid)
+def test_parity_list_rounds(gc, tuning):
     """List rounds (bounded degree <= 64, 8-bit words): entered from dense, sparse or switch rounds."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
     for g in (wl.mesh2d(100, 77, 0.3), wl.mesh2d(64, 64), wl.stencil27(9, 7, 5), wl.stencil27(12),
               wl.gnp(400, 0.02, 3), wl.path(1000), wl.cycle(999), wl.rmat(12, 2, wl.RMAT_ER)):
         assert g.max_degree() <= 64
         for pol in POLICIES:
-            _check(gc, g, pol)
+            _check(gc, g, pol, tuning=tuning)
+
+
+def test_bad_tuning_rejected(gc):
+    rp, ci = _dev(wl.path(10))
+    with pytest.raises(gc.GcError) as e:
+        gc.color(rp, ci, tuning=dict(state_bytes=3))
+    assert e.value.status == 1
 
 
 @pytest.mark.parametrize("k", [126, 127, 128, 129, 136])
 def test_state_word_restart(gc, k):
     """8-bit state words hold colours <= 127: K_k needs colour k, so K_128 and beyond are
-    restarted with 16-bit words; colours up to 128 come from the 16 forbidden-colour planes,
+    restarted with 16-bit words; colours up to 512 come from the 64 forbidden-colour planes,
     beyond from the windowed fallback (reading C7)."""
     res = _check(gc, wl.complete(k))
     assert res.num_colors == k
