@@ -154,15 +154,65 @@ def measured_peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f), "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0}, "fallback"
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg):
+def ncu_record(cfg):
+    """ncu numbers of the persistent kernel for this config from profiles/ncu_traffic.json
+    (written by scripts/ncu_record.py from an `ncu --set full` capture, stamped with the
+    commit it profiled)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(cfg)
+            rec = json.load(f)
     except Exception:
         return None
+    r = rec.get("configs", {}).get(cfg)
+    if r is None:
+        return None
+    return dict(r, commit=rec.get("commit"))
+
+
+def git_commit():
+    try:
+        import subprocess
+        return subprocess.run(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                              text=True, timeout=10).stdout.strip() or None
+    except Exception:
+        return None
+
+
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+RMAT_CFG = {"rmat16": (16, 8), "rmat24": (24, 16), "rmat27": (27, 16)}
+
+
+def golden(cfg, policy):
+    """The oracle's result for this workload (tests/golden, written by scripts/make_goldens.py,
+    which calls only oracle/)."""
+    try:
+        with open(os.path.join(GOLDEN_DIR, f"oracle_{cfg}_{policy}.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def colour_sha(c_u32):
+    import hashlib
+
+    import numpy as np
+    return hashlib.sha256(np.ascontiguousarray(c_u32, dtype="<u4").tobytes()).hexdigest()
+
+
+def device_graph(cfg, device):
+    """(row_ptr, col_idx) of a BASELINE config on `device` (R-MAT built on the GPU: identical
+    to the CPU generator, tests/test_workloads.py)."""
+    import torch
+
+    import workloads as wl
+    if cfg in RMAT_CFG:
+        s, ef = RMAT_CFG[cfg]
+        return wl.rmat_range_gpu(s, ef, 0, 1 << s, device=device)
+    g = wl.config_graph(cfg)
+    return torch.from_numpy(g.row_ptr).to(device), torch.from_numpy(g.col_idx).to(device)
 
 
 def run_reference(args):
@@ -171,8 +221,6 @@ def run_reference(args):
         return 0
     import oracle  # noqa: F401  (the reference arm is the CPU oracle)
     g, desc = sample_graph(args.config)
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state; warm-up steps are not repeated for the CPU arm
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -186,67 +234,128 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "sample": desc, "n": g.n, "m": g.m, "policy": "higher_id"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{desc}: n={g.n} m={g.m}, oracle_sgr single-threaded C, mean of {args.steps}"},
+                         "sample": f"{desc}: n={g.n} m={g.m}, oracle_sgr single-threaded C, mean of {args.steps} "
+                                   "(warm-up steps not repeated: the oracle keeps no state)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_partitioned(args, g, rank, world, local):
-    """N > 1: one edge-balanced vertex range per rank, replicated ghost state, two NCCL
-    all-gathers per round (paper_1606_06025_b200.dist) — strong scaling on one graph."""
+def run_partitioned(args, rank, world, local):
+    """N > 1: one vertex range per rank, one persistent kernel per GPU with the device-initiated
+    exchange (include/gc_dist.h); torch.distributed only broadcasts the NCCL id and gathers the
+    colours for the parity check after the timed region."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1606_06025_b200 as gc
-    from paper_1606_06025_b200.dist import CudaPartition, TorchComm, local_slice, run_rounds
+    import paper_1606_06025_b200.dist as gd
+    import workloads as wl
 
-    n, m = g.n, g.m
-    bounds = gc.partition_edge_balanced(g.row_ptr, world)
-    b, e = int(bounds[rank]), int(bounds[rank + 1])
-    rpl, cil = local_slice(g.row_ptr, g.col_idx, b, e)
-    rpl = torch.from_numpy(rpl.copy()).cuda()
-    cil = torch.from_numpy(cil.copy() if len(cil) else np.zeros(1, np.int32)).cuda()
-    comm = TorchComm()
-
-    def step():
-        part = CudaPartition(n, b, e, rpl, cil, args.policy)
-        res = run_rounds([part], comm)
-        part.close()
-        return res
-
+    dev = torch.device("cuda", local)
+    if args.config in RMAT_CFG:
+        # each rank builds only its own rows on its GPU; ranges uniform in vertex id (the seeded
+        # relabelling spreads the degrees evenly: edge imbalance reported below)
+        s, ef = RMAT_CFG[args.config]
+        n = 1 << s
+        bounds = [n * k // world for k in range(world + 1)]
+        b, e = bounds[rank], bounds[rank + 1]
+        rpl, cil = wl.rmat_range_gpu(s, ef, b, e, device=dev)
+        partition = "uniform vertex ranges (seeded relabelling)"
+    else:
+        g = wl.config_graph(args.config)
+        n = g.n
+        bounds = [int(x) for x in gc.partition_edge_balanced(g.row_ptr, world)]
+        b, e = bounds[rank], bounds[rank + 1]
+        rpl, cil = gd.local_slice(g.row_ptr, g.col_idx, b, e)
+        rpl, cil = torch.from_numpy(rpl.copy()).to(dev), torch.from_numpy(cil.copy()).to(dev)
+        partition = "edge-balanced vertex ranges"
+    m_local = torch.tensor([int(rpl[-1])], device=dev, dtype=torch.int64)
+    ms_all = [torch.zeros_like(m_local) for _ in range(world)]
+    dist.all_gather(ms_all, m_local)
+    m_ranks = [int(x.item()) for x in ms_all]
+    m = sum(m_ranks)
+    comm = gd.init_from_torch(local)
+    out = torch.empty(max(e - b, 1), dtype=torch.int32, device=dev)
+    kw = dict(policy=args.policy, validate=False, out=out)
     for _ in range(args.warmup):
-        res = step()
+        gd.color_dist(comm, n, b, e, rpl, cil, **kw)
     clocks = ClockSampler(local).start()
     dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    kms = []
     for _ in range(args.steps):
-        res = step()
+        r = gd.color_dist(comm, n, b, e, rpl, cil, time_kernel=True, **kw)
+        kms.append(r.kernel_ms)
+    e1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    dt = (time.perf_counter() - t0) / args.steps
     clk = clocks.stop()
-    t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps, sum(kms) / len(kms)], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) * 1e3
+    ms, kernel_ms = float(t[0]), float(t[1])
+    res = gd.color_dist(comm, n, b, e, rpl, cil, trace=True, **kw)
+    # e2e: the same call with this rank's rows and colours in pinned HOST memory
+    e2e = None
+    if not args.no_e2e:
+        h_rp, h_ci = rpl.cpu().pin_memory(), cil.cpu().pin_memory()
+        h_out = torch.empty(max(e - b, 1), dtype=torch.int32).pin_memory()
+        gd.color_dist(comm, n, b, e, h_rp.numpy(), h_ci.numpy(), policy=args.policy, validate=False,
+                      out=h_out.numpy().view(np.uint32))
+        dist.barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 5))
+        for _ in range(e2e_steps):
+            gd.color_dist(comm, n, b, e, h_rp.numpy(), h_ci.numpy(), policy=args.policy, validate=False,
+                          out=h_out.numpy().view(np.uint32))
+        dist.barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": m / float(te[0]) / 1e9, "unit": UNIT, "ms_per_step": float(te[0]) * 1e3,
+               "h2d_bytes_per_step": 8 * (n + world) + 4 * m, "d2h_bytes_per_step": 4 * n,
+               "timing": "host wall clock between barriers, max over ranks (every call is synchronous)"}
+    # parity after the timed region: gather the colour ranges to rank 0
+    sizes = [bounds[k + 1] - bounds[k] for k in range(world)]
+    mx = max(sizes)
+    mine = torch.zeros(mx, dtype=torch.int32, device=dev)
+    mine[:e - b] = out[:e - b]
+    allc = [torch.zeros(mx, dtype=torch.int32, device=dev) for _ in range(world)]
+    dist.all_gather(allc, mine)
+    parity = {}
+    if rank == 0:
+        colors = np.concatenate([allc[k][:sizes[k]].cpu().numpy().view(np.uint32) for k in range(world)])
+        gdn = golden(args.config, args.policy)
+        parity["bit_exact_vs_oracle"] = (None if gdn is None else
+                                         bool(colour_sha(colors) == gdn["sha256_colors_u32le"]
+                                              and res.rounds == gdn["rounds"] and res.num_colors == gdn["num_colors"]
+                                              and res.trace == gdn["trace"]))
+        if args.config != "rmat27":  # one-GPU reference run on rank 0's GPU
+            rp1, ci1 = device_graph(args.config, dev)
+            one = gc.color(rp1, ci1, policy=args.policy, validate=False)
+            parity["bit_exact_vs_1gpu"] = bool(np.array_equal(one.colors.cpu().numpy().view(np.uint32), colors)
+                                               and one.rounds == res.rounds and one.num_colors == res.num_colors)
+            del rp1, ci1
+    comm.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": m / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": args.config, "n": n, "m": m, "policy": args.policy,
-                       "parallelism": f"vertex-range partitions x{world} (edge-balanced), NCCL all-gather",
+                       "parallelism": f"{partition} x{world}: one persistent kernel per GPU, device-initiated "
+                                      "exchange over NVLink peer memory (include/gc_dist.h)",
+                       "edge_imbalance": max(m_ranks) / (m / world) - 1.0,
                        "l2": "inputs larger than L2; no flush"},
-            "num_colors": res.num_colors, "rounds": res.rounds,
-            "exchanged_pairs_rank0": res.exchanged_pairs,
-            "timing": "host wall clock between barriers (every dist call is synchronous), max over ranks",
-            # per step: create (fill, 2 ingest, halo count, CUB scan (2), halo fill = 7); round 1:
-            # phase B + pack + unpack + halo apply; rounds >= 2: 8 (phase A, pack, unpack, halo
-            # apply, phase B, pack, unpack, halo apply); finalize 1
-            "gpu_launches": args.steps * (7 + 4 + 8 * (res.rounds - 1) + 1), "clocks": clk,
+            "num_colors": res.num_colors, "rounds": res.rounds, **parity,
+            "kernel_ms_max_over_ranks": kernel_ms,
+            "timing": "CUDA events on each rank's stream around the timed steps, max over ranks",
+            "e2e": e2e,
+            "gpu_launches": args.steps * 1,  # per step and rank: the persistent kernel
+            "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -257,7 +366,6 @@ def run_ours(args):
     import torch
 
     import paper_1606_06025_b200 as gc
-    import workloads as wl
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -265,32 +373,33 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            return run_partitioned(args, rank, world, local)
+        finally:
+            dist.destroy_process_group()
 
-    g = wl.config_graph(args.config)
-    n, m = g.n, g.m
-    if world > 1:
-        ret = run_partitioned(args, g, rank, world, local)
-        dist.destroy_process_group()
-        return ret
-    rp = torch.from_numpy(g.row_ptr).cuda()
-    ci = torch.from_numpy(g.col_idx).cuda()
+    rp, ci = device_graph(args.config, torch.device("cuda", local))
+    n, m = int(rp.shape[0]) - 1, int(rp[-1])
     out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     kw = dict(policy=args.policy, validate=False, out=out)
 
     # untimed instrumented run: exact work counters -> algorithmic bytes per launch
     wres = gc.color(rp, ci, count_work=True, trace=True, **kw)
     work = wres.work
-    alg_bytes = algorithmic_bytes(work, n)
-    sv_bytes = survey_bytes(work, n, m)
+    design_bytes = algorithmic_bytes(work, n)
+    alg_bytes = survey_bytes(work, n, m)
     verified = gc.verify(rp, ci, out) == -1
+    c = out[:n].cpu().numpy().view(np.uint32)
+    gdn = golden(args.config, args.policy)
+    bit_exact = (None if gdn is None else
+                 bool(colour_sha(c) == gdn["sha256_colors_u32le"] and wres.rounds == gdn["rounds"]
+                      and wres.num_colors == gdn["num_colors"] and wres.trace == gdn["trace"]))
 
     for _ in range(args.warmup):
         gc.color(rp, ci, **kw)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local).start()
-    if dist:
-        dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     kms = []
@@ -299,23 +408,17 @@ def run_ours(args):
         kms.append(r.kernel_ms)
     e1.record(stream)
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     kernel_ms = sum(kms) / len(kms)
-    value = world * m / (ms / 1e3) / 1e9
+    value = m / (ms / 1e3) / 1e9
 
     # e2e: the same call with pinned HOST buffers (H2D of the CSR and D2H of the colours
     # inside the timed region, done by the library)
     e2e = None
     if not args.no_e2e:
-        h_rp = torch.from_numpy(g.row_ptr).pin_memory()
-        h_ci = torch.from_numpy(g.col_idx).pin_memory()
+        h_rp = rp.cpu().pin_memory()
+        h_ci = ci.cpu().pin_memory()
         h_out = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
         h_rp_np, h_ci_np, h_out_np = h_rp.numpy(), h_ci.numpy(), h_out.numpy().view(np.uint32)
         e2e_steps = max(1, min(args.steps, 10))
@@ -325,50 +428,63 @@ def run_ours(args):
         for _ in range(e2e_steps):
             gc.color(h_rp_np, h_ci_np, policy=args.policy, validate=False, out=h_out_np)
         e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
-        assert np.array_equal(h_out_np[:n], out.cpu().numpy().view(np.uint32)[:n])
+        assert np.array_equal(h_out_np[:n], c)
         e2e = {"value": m / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 8 * (n + 1) + 4 * m, "d2h_bytes_per_step": 4 * n + 224}
+        del h_rp, h_ci
 
     peaks, src = measured_peaks()
     peak = float(peaks["hbm_gbs"])
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-    achieved_survey = sv_bytes / (kernel_ms / 1e3) / 1e9
-    traffic = ncu_traffic(args.config)
+    achieved_design = design_bytes / (kernel_ms / 1e3) / 1e9
+    nrec = ncu_record(args.config)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if not args.no_cpu:
         cpu = cpu_oracle_gteps(args.config)
+    if args.cpu_full:  # the oracle on the bench graph itself (minutes at s24)
+        import oracle
+        import workloads as wl
+        g = wl.config_graph(args.config)
+        t0 = time.perf_counter()
+        cf, _, _ = oracle.sgr(g, args.policy)
+        dtf = time.perf_counter() - t0
+        cpu = dict(cpu or {}, full_graph={"value": g.m / dtf / 1e9, "unit": UNIT, "seconds": dtf, "cores": 1,
+                                          "bit_exact": bool(np.array_equal(cf, c))})
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u%d" % (8 * int(work.get("state_bytes") or 4)),
-            "data": "synthetic",
-            "config": {"workload": args.config, "n": n, "m": m, "policy": args.policy,
-                       "validate": False, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
-                       "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB); no flush" % ((8 * (n + 1) + 4 * m) / 1e9)},
-            "num_colors": wres.num_colors, "rounds": wres.rounds, "verified_ff_fixpoint": verified,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": f"{src} hbm_gbs", "kernel": "sgr_persistent",
-                         "kernel_ms": kernel_ms,
-                         "alg_bytes_per_launch": alg_bytes,
-                         "alg_bytes_model": "this design's per-unit bytes x exact unit counts (DESIGN.md 5.3, 7)",
-                         "survey_bytes_per_launch": sv_bytes,
-                         "survey_effective_gbs": achieved_survey,
-                         "survey_effective_frac": achieved_survey / peak},
-            "work": work,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            # per step: the persistent kernel, plus the max-degree pre-pass that selects the
-            # kernel variant when the graph has >= 8 entries per row (gc_api.cu)
-            "gpu_launches": args.steps * (2 if m >= 8 * n else 1),
-            "clocks": clk,
-        }
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u%d" % (8 * int(work.get("state_bytes") or 4)),
+        "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "m": m, "policy": args.policy,
+                   "validate": False, "parallelism": "1gpu",
+                   "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB); no flush" % ((8 * (n + 1) + 4 * m) / 1e9)},
+        "num_colors": wres.num_colors, "rounds": wres.rounds, "verified_ff_fixpoint": verified,
+        "bit_exact_vs_oracle": bit_exact,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak,
+                     "traffic": nrec.get("dram_bytes") if nrec else None,
+                     "traffic_commit": nrec.get("commit") if nrec else None,
+                     "peak_source": f"{src} hbm_gbs", "kernel": "sgr_persistent",
+                     "kernel_ms": kernel_ms,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "alg_bytes_model": "SURVEY 8(d): sum_r sum_{v in W_r} (24 + 8 deg v) + (28 + 8 s_B(v)), "
+                                        "exact unit counts of this launch (s_B in this design's scan order)",
+                     "design_bytes_per_launch": design_bytes,
+                     "design_bytes_frac": achieved_design / peak,
+                     "ncu_dram_frac": (nrec["dram_bytes"] / (nrec["kernel_ms"] / 1e3) / 1e9 / peak) if nrec else None,
+                     "ncu": nrec},
+        "work": work,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        # per step: the persistent kernel, plus the max-degree pre-pass that selects the
+        # kernel variant when the graph has >= 8 entries per row (gc_api.cu)
+        "gpu_launches": args.steps * (2 if m >= 8 * n else 1),
+        "clocks": clk,
+        "commit": git_commit(),
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -382,6 +498,7 @@ def main():
     ap.add_argument("--policy", default="higher_id")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="also time the oracle on the bench graph itself")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

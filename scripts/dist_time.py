@@ -1,26 +1,36 @@
-import os, sys, time
+"""Time the multi-GPU kernels in the one-process emulation (all ranks on one GPU; diagnostics,
+not a scaling number): per P, the slowest rank's kernel time of gc_color_dist and whether the
+colours equal one-GPU gc_color's.
+
+    python scripts/dist_time.py rmat24 [P ...]
+"""
+import os
+import sys
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # emulated ranks: one hardware queue each
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch, workloads as wl, paper_1606_06025_b200 as gc
-from paper_1606_06025_b200.dist import CudaPartition, LocalComm, local_slice, run_rounds
-cfg = sys.argv[1]
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1606_06025_b200 as gc  # noqa: E402
+import paper_1606_06025_b200.dist as d  # noqa: E402
+import workloads as wl  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "rmat24"
+parts_list = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
 g = wl.config_graph(cfg)
-rp = torch.from_numpy(g.row_ptr).cuda(); ci = torch.from_numpy(g.col_idx).cuda()
-ref = gc.color(rp, ci, validate=False)
-for parts in (1, 2):
-    for rep in range(2):
-        bounds = gc.partition_edge_balanced(g.row_ptr, parts)
-        torch.cuda.synchronize(); t0 = time.perf_counter()
-        objs = []
-        for k in range(parts):
-            b, e = int(bounds[k]), int(bounds[k + 1])
-            rpl, cil = local_slice(rp, ci, b, e)
-            objs.append(CudaPartition(g.n, b, e, rpl.contiguous(), cil.contiguous()))
-        torch.cuda.synchronize(); t1 = time.perf_counter()
-        res = run_rounds(objs, LocalComm())
-        torch.cuda.synchronize(); t2 = time.perf_counter()
-        c = torch.cat(res.colors_local)
-        for o in objs:
-            o.close()
-        torch.cuda.synchronize(); t3 = time.perf_counter()
-        print(cfg, "parts", parts, "create %.1f ms rounds %.1f ms close %.1f ms" % ((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3),
-              "rounds", res.rounds, "same", bool(torch.equal(c.cuda(), ref.colors)), flush=True)
+rp = torch.from_numpy(g.row_ptr).cuda()
+ci = torch.from_numpy(g.col_idx).cuda()
+one = gc.color(rp, ci, validate=False, time_kernel=True)
+ref = one.colors.cpu().numpy().view(np.uint32)
+print(cfg, "1 GPU gc_color kernel %.2f ms" % one.kernel_ms, flush=True)
+for parts in parts_list:
+    bounds = gc.partition_edge_balanced(g.row_ptr, parts)
+    comms = d.local_group(parts)
+    for rep in range(3):
+        colors, res = d.color_partitioned_local(rp, ci, bounds, comms=comms, validate=False, time_kernel=True)
+        print(cfg, "P", parts, "rep", rep, "slowest rank kernel %.2f ms" % max(r.kernel_ms for r in res),
+              "rounds", res[0].rounds, "same", bool(np.array_equal(colors, ref)), flush=True)
+    for c in comms:
+        c.close()

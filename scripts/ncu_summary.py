@@ -15,10 +15,26 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
         "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_read.sum",
         "lts__t_sectors_op_write.sum"]
+def find(w):
+    """Column of metric w: exact name, else a prefixed variant (this ncu reports e.g.
+    FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed), else the .ratio
+    form of a .pct metric (smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio)."""
+    cands = [w] + ([w[:-4] + ".ratio"] if w.endswith(".pct") else [])
+    for c in cands:
+        if c in hdr:
+            return hdr.index(c), c
+        for i, h in enumerate(hdr):
+            if h.endswith("." + c) or h.endswith(c):
+                return i, h
+    return None, None
+
+
 for w in want:
-    if w in hdr:
-        i = hdr.index(w)
-        print(f"{w:65s} {vals[i]:>20s} {units[i]}")
+    i, name = find(w)
+    if i is None:
+        print(f"{w:65s} {'(not reported)':>20s}")
+    else:
+        print(f"{name:65s} {vals[i]:>20s} {units[i]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))

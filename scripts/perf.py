@@ -43,20 +43,17 @@ def main():
     variants["modes"] = [dict(), dict(pull_firstfit=True), dict(host_rounds=True),
                          dict(host_rounds=True, pull_firstfit=True)]
     variants["policy"] = [dict(policy=p) for p in ("higher_id", "lower_id", "degree")]
-    variants["compact"] = [dict(), dict(env={"GC_COMPACT": "1"}), dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "16"}),
-                           dict(env={"GC_COMPACT": "1", "GC_DENSE_DIV": "64"})]
-    variants["n1chg"] = [dict(), dict(env={"GC_N1": "0", "GC_DENSE_DIV": "16"}), dict(env={"GC_N1_CHG": "2"}),
-                         dict(env={"GC_N1_CHG": "4"}), dict(env={"GC_N1_CHG": "8"}), dict(env={"GC_N1_CHG": "16"})]
-    variants["list"] = [dict(env={"GC_LIST": x}) for x in ("0", "1", "2")]
-    variants["n1"] = [dict(env={"GC_N1": x}) for x in ("0", "1", "2")]
-    variants["dense"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("0", "2", "4", "8", "16", "64")]
+    T = lambda **t: dict(tuning=t)  # noqa: E731  (gc_tuning overrides)
+    variants["compact"] = [dict(), T(compact=1), T(compact=1, dense_div=16), T(compact=1, dense_div=64)]
+    variants["n1chg"] = [dict(), T(n1=0, dense_div=16)] + [T(n1_chg=x) for x in (2, 4, 8, 16)]
+    variants["list"] = [T(list=x) for x in (0, 1, 2)]
+    variants["n1"] = [T(n1=x) for x in (0, 1, 2)]
+    variants["dense"] = [T(dense_div=d) for d in (0, 2, 4, 8, 16, 64)]
     variants["t3"] = [dict(warp_bin_max=t) for t in (512, 768, 1024, 1536, 2048)]
-    variants["dch"] = [dict(env={"GC_DCH": d}) for d in ("2", "4", "8", "16", "32")]
-    variants["div"] = [dict(env={"GC_DENSE_DIV": d}) for d in ("2", "3", "4", "6")]
-    variants["densen1"] = [dict(env={"GC_DENSE_DIV": d, "GC_N1": "2"}) for d in ("4", "8", "16", "32", "64", "256")]
-    variants["env"] = [dict(), dict(env={"GC_SCATTER_FILTER": "1"}), dict(env={"GC_STATE_BYTES": "2"}),
-                       dict(env={"GC_L2_PERSIST": "0"}), dict(env={"GC_L2_PLANES": "1"}),
-                       dict(env={"GC_L2_PLANES": "2"}), dict(env={"GC_SCATTER_FILTER": "1", "GC_L2_PLANES": "1"})]
+    variants["dch"] = [T(dch=d) for d in (2, 4, 8, 16, 32)]
+    variants["div"] = [T(dense_div=d) for d in (2, 3, 4, 6)]
+    variants["densen1"] = [T(dense_div=d, n1=2) for d in (4, 8, 16, 32, 64, 256)]
+    variants["misc"] = [dict(), T(scatter_filter=1), T(state_bytes=2), T(variant=0), T(variant=1)]
     if args.sweep == "phases":
         res = gc.color(rp, ci, validate=False, phase_times=True)
         tot_a = sum(a for a, b in res.phase_us)
@@ -68,9 +65,6 @@ def main():
         return
     for kw in variants[args.sweep]:
         kw = dict(kw)
-        env = kw.pop("env", {})
-        old = {k: os.environ.get(k) for k in env}
-        os.environ.update(env)
         ts = []
         res = None
         for _ in range(args.reps):
@@ -78,12 +72,6 @@ def main():
             ts.append(res.kernel_ms)
         ms = statistics.median(ts)
         same = bool(torch.equal(res.colors, ref_c)) if "policy" not in kw else None
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
-        kw.update(env)
         print(json.dumps({"config": args.config, "kw": kw, "kernel_ms": round(ms, 4),
                           "gteps": round(g.m / ms / 1e6, 3), "rounds": res.rounds,
                           "colors": res.num_colors, "same_as_default": same}), flush=True)

@@ -230,16 +230,3 @@ def test_stencil128_config1_closed_form(gc):
     expect = (1 + (x % 2) + 2 * (y % 2) + 4 * (z % 2)).to(torch.int32)
     assert torch.equal(res.colors, expect)
     assert res.num_colors == 8 and res.rounds == 197
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("name", ["stencil128", "mesh8192", "rmat24"])
-def test_full_size_configs_vs_oracle(gc, name):
-    """Full BASELINE.json configs, bit-exact vs the oracle (minutes of CPU for rmat24)."""
-    g = wl.config_graph(name)
-    rp, ci = _dev(g)
-    res = gc.color(rp, ci, validate=True)
-    c = _gpu_colors(res)
-    assert gc.verify(rp, ci, res.colors) == -1
-    c_ref, nc, r = oracle.sgr(g)
-    assert np.array_equal(c, c_ref) and res.num_colors == nc and res.rounds == r

@@ -108,3 +108,15 @@ def test_rmat_range_equals_whole_graph(bounds):
         rp, ci = wl.rmat_range(12, 16, b, e)
         assert np.array_equal(rp, g.row_ptr[b:e + 1] - g.row_ptr[b])
         assert np.array_equal(ci, g.col_idx[g.row_ptr[b]:g.row_ptr[e]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale,ef,abc,seed", [(10, 8, wl.RMAT_G, 1), (12, 16, wl.RMAT_G, 1), (11, 16, wl.GRAPH500, 5),
+                                               (14, 8, wl.RMAT_ER, 3)])
+def test_rmat_range_gpu_equals_cpu(scale, ef, abc, seed):
+    """The GPU generator (gen_gpu.cu) builds exactly gen.c's rows, for any range and chunking."""
+    n = 1 << scale
+    for (b, e), chunk in (((0, n), 1 << 29), ((0, n), 997), ((n // 3, n - 5), 4096), ((7, 7), 1 << 20)):
+        rp, ci = wl.rmat_range(scale, ef, b, e, abc, seed)
+        rpg, cig = wl.rmat_range_gpu(scale, ef, b, e, abc, seed, chunk_arcs=chunk)
+        assert np.array_equal(rpg.cpu().numpy(), rp) and np.array_equal(cig.cpu().numpy(), ci), (b, e, chunk)

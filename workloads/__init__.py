@@ -19,16 +19,26 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen.c")
 _LIB = os.path.join(_HERE, "libgcgen.so")
+_SRC_GPU = os.path.join(_HERE, "gen_gpu.cu")
+_LIB_GPU = os.path.join(_HERE, "libgcgen_gpu.so")
 _lib = None
+_lib_gpu = None
 
 
-def build(force: bool = False) -> str:
-    """Compile gen.c into libgcgen.so (gcc -O3 -fopenmp)."""
+def build(force: bool = False, gpu: bool = True) -> str:
+    """Compile gen.c into libgcgen.so (gcc -O3 -fopenmp) and gen_gpu.cu into libgcgen_gpu.so
+    (nvcc, sm_100a)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-fPIC", "-shared",
                                "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
+    if gpu and (force or not os.path.exists(_LIB_GPU) or os.path.getmtime(_LIB_GPU) < os.path.getmtime(_SRC_GPU)):
+        tmp = _LIB_GPU + f".tmp{os.getpid()}"
+        nvcc = "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc"
+        subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+                               "-shared", "-o", tmp, _SRC_GPU])
+        os.replace(tmp, _LIB_GPU)
     return _LIB
 
 
@@ -49,6 +59,8 @@ def _load():
                                    i64p, i64p, i64pp, i32pp]
         lib.gen_from_edges.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int64, i64p, i64pp, i32pp]
+        lib.gen_rmat_perm.argtypes = [ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p]
+        lib.gen_rmat_perm.restype = ctypes.c_int
         lib.gen_splitmix64.argtypes = [ctypes.c_uint64]
         lib.gen_splitmix64.restype = ctypes.c_uint64
         lib.gen_free.argtypes = [ctypes.c_void_p]
@@ -131,6 +143,75 @@ def rmat_range(scale: int, edge_factor: int, v_begin: int, v_end: int, abc=RMAT_
     if rc != 0:
         raise ValueError(f"gen_rmat_range failed with code {rc}")
     return _adopt(rp, v_end - v_begin + 1, np.int64), _adopt(ci, m.value, np.int32)
+
+
+def rmat_perm(scale: int, seed: int = 1) -> np.ndarray:
+    """The seeded Fisher-Yates relabelling of the W1 recipe (int32[2^scale])."""
+    pi = np.empty(1 << scale, dtype=np.int32)
+    rc = _load().gen_rmat_perm(scale, seed, pi.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"gen_rmat_perm failed with code {rc}")
+    return pi
+
+
+def _load_gpu():
+    global _lib_gpu
+    if _lib_gpu is None:
+        build()
+        lib = ctypes.CDLL(_LIB_GPU)
+        lib.gen_rmat_emit_gpu.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_ulonglong, ctypes.c_void_p, ctypes.c_longlong,
+                                          ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                          ctypes.c_void_p]
+        lib.gen_rmat_emit_gpu.restype = ctypes.c_int
+        _lib_gpu = lib
+    return _lib_gpu
+
+
+def rmat_range_gpu(scale: int, edge_factor: int, v_begin: int, v_end: int, abc=RMAT_G, seed: int = 1,
+                   device="cuda", chunk_arcs: int = 1 << 29):
+    """Rows [v_begin, v_end) of rmat(scale, edge_factor, abc, seed), built on the GPU:
+    (row_ptr int64[v_end-v_begin+1] rebased to 0, col_idx int32, global ids) as torch tensors on
+    `device`.  Identical to rmat_range (tests/test_workloads.py).  Rows are produced in vertex
+    chunks of at most about chunk_arcs arcs (each chunk: count pass, emit pass, sort, dedupe)."""
+    import torch
+    lib = _load_gpu()
+    a, b, c = abc
+    ab, abc_ = a + b, a + b + c
+    n = 1 << scale
+    ns = edge_factor * n
+    dev = torch.device(device)
+    pi = torch.from_numpy(rmat_perm(scale, seed)).to(dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def arcs(cb, ce, keys=None):
+        cnt.zero_()
+        rc = lib.gen_rmat_emit_gpu(scale, ns, a, ab, abc_, seed, pi.data_ptr(), cb, ce, cnt.data_ptr(),
+                                   keys.data_ptr() if keys is not None else None,
+                                   keys.numel() if keys is not None else 0, stream)
+        if rc != 0:
+            raise RuntimeError(f"gen_rmat_emit_gpu: cudaError {rc}")
+        return int(cnt.item())
+
+    total = arcs(v_begin, v_end)
+    nchunks = max(1, -(-total // chunk_arcs))
+    cuts = [v_begin + (v_end - v_begin) * k // nchunks for k in range(nchunks + 1)]
+    degs, cols = [], []
+    for cb, ce in zip(cuts[:-1], cuts[1:]):
+        k = arcs(cb, ce)
+        keys = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+        assert arcs(cb, ce, keys) == k
+        keys = torch.unique_consecutive(torch.sort(keys[:k]).values)
+        degs.append(torch.bincount(keys >> 32, minlength=ce - cb) if k else torch.zeros(ce - cb, dtype=torch.int64,
+                                                                                          device=dev))
+        cols.append((keys & 0xFFFFFFFF).to(torch.int32) if k else torch.zeros(0, dtype=torch.int32, device=dev))
+        del keys
+    rp = torch.zeros(v_end - v_begin + 1, dtype=torch.int64, device=dev)
+    if v_end > v_begin:
+        torch.cumsum(torch.cat(degs), 0, out=rp[1:])
+    ci = torch.cat(cols) if cols else torch.zeros(0, dtype=torch.int32, device=dev)
+    return rp, ci
 
 
 def stencil27(nx: int, ny: int | None = None, nz: int | None = None) -> Graph:

@@ -174,6 +174,19 @@ static inline void rmat_sample(int32_t scale, uint64_t base, int64_t i, double a
   *v_out = v;
 }
 
+/* The seeded Fisher-Yates relabelling pi of gen_rmat_range (pi_out: int32[2^scale]); the GPU
+ * generator (gen_gpu.cu) takes it as input so both sides use one permutation routine. */
+int gen_rmat_perm(int32_t scale, uint64_t seed, int32_t* pi_out) {
+  if (scale < 1 || scale > 30 || !pi_out) return 1;
+  const int64_t n = (int64_t)1 << scale;
+  for (int64_t i = 0; i < n; ++i) pi_out[i] = (int32_t)i;
+  for (int64_t i = n - 1; i >= 1; --i) {
+    uint64_t j = splitmix64((seed ^ 0x5851F42D4C957F2DULL) + (uint64_t)(n - 1 - i)) % (uint64_t)(i + 1);
+    int32_t t = pi_out[i]; pi_out[i] = pi_out[j]; pi_out[j] = t;
+  }
+  return 0;
+}
+
 int gen_rmat_range(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
                    int64_t vb, int64_t ve, int64_t* m_out, int64_t** row_ptr_out, int32_t** col_out) {
   if (scale < 1 || scale > 30 || edge_factor < 0) return 1;
@@ -185,11 +198,7 @@ int gen_rmat_range(int32_t scale, int64_t edge_factor, double a, double b, doubl
   int64_t* off = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
   int64_t* cur = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
   if (!pi || !off || !cur) { free(pi); free(off); free(cur); return 2; }
-  for (int64_t i = 0; i < n; ++i) pi[i] = (int32_t)i;
-  for (int64_t i = n - 1; i >= 1; --i) {
-    uint64_t j = splitmix64((seed ^ 0x5851F42D4C957F2DULL) + (uint64_t)(n - 1 - i)) % (uint64_t)(i + 1);
-    int32_t t = pi[i]; pi[i] = pi[j]; pi[j] = t;
-  }
+  gen_rmat_perm(scale, seed, pi);
   const double ab = a + b, abc = a + b + c;
   const uint64_t base = seed << 40;
   /* pass 1: arcs per local row (both directions of every non-loop sample, duplicates kept) */
