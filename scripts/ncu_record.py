@@ -18,9 +18,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def col(hdr, name):
+def col(hdr, name, vals=None):
+    """Exact metric name first, else a section-prefixed variant that has a value."""
+    if name in hdr:
+        return hdr.index(name)
     for i, h in enumerate(hdr):
-        if h == name or h.endswith("." + name) or h.endswith(name):
+        if h.endswith("." + name) and (vals is None or vals[i]):
             return i
     return None
 
@@ -33,7 +36,7 @@ def main():
     hdr, units, vals = rows[0], rows[1], rows[2]
 
     def get(name, scale=1.0):
-        i = col(hdr, name)
+        i = col(hdr, name, vals)
         if i is None or not vals[i]:
             return None
         v = float(vals[i].replace(",", ""))
@@ -56,7 +59,8 @@ def main():
     rec = {
         "dram_bytes": (rd or 0) + (wr or 0), "dram_read_bytes": rd, "dram_write_bytes": wr,
         "kernel_ms": get("gpu__time_duration.sum"),
-        "dram_throughput_pct": get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+        "dram_throughput_pct": get("dram__throughput.avg.pct_of_peak_sustained_elapsed")
+        or get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         "l2_hit_pct": get("lts__t_sector_hit_rate.pct"),
         "l2_throughput_pct": get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
         "l2_sectors": get("lts__t_sectors.sum"),
