@@ -478,9 +478,8 @@ def run_ours(args):
         "work": work,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # per step: the persistent kernel, plus the max-degree pre-pass that selects the
-        # kernel variant when the graph has >= 8 entries per row (gc_api.cu)
-        "gpu_launches": args.steps * (2 if m >= 8 * n else 1),
+        # per step: the persistent kernel (the variant choice comes from the previous call)
+        "gpu_launches": args.steps,
         "clocks": clk,
         "commit": git_commit(),
     }

@@ -24,9 +24,11 @@
  *  - On error every scalar output is set to 0, array outputs are unspecified, nothing is
  *    thrown or aborted, and a human-readable detail is available from
  *    gc_last_error_message() (thread-local).
- *  - No global mutable state other than a per-device workspace memory pool and per-device
- *    attribute caches; no device- or context-wide setting (L2 limits, access-policy windows,
- *    ...) is changed.  Concurrent calls on distinct streams are allowed.
+ *  - No global mutable state other than a per-device workspace memory pool, per-device
+ *    attribute caches and a small cache of the kernel variant chosen for recently seen graphs
+ *    (keyed by device, row_ptr address, n and m; it affects speed only, never the result);
+ *    no device- or context-wide setting (L2 limits, access-policy windows, ...) is changed.
+ *    Concurrent calls on distinct streams are allowed.
  *  - No tuning choice is read from the environment: they are all in gc_opts / gc_tuning.
  */
 #ifndef GC_H_

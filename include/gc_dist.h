@@ -55,12 +55,11 @@ gc_status gc_comm_init(gc_comm** out, int32_t rank, int32_t world, const void* n
                        int32_t device);
 
 /* One-process emulation (tests, one GPU): comms_out[world] communicators whose ranks all live
- * on `device` and bootstrap through memory instead of NCCL.  The kernels, windows, peer stores
- * and cross-rank barriers are the multi-GPU ones; each rank's gc_color_dist must be called
- * concurrently from its own host thread (the ranks' persistent kernels run side by side, each
- * on 1/world of the SMs).  The ranks' streams must not share a hardware queue: world > 1 needs
- * CUDA_DEVICE_MAX_CONNECTIONS >= 2 x world in the environment before CUDA initialises
- * (else GC_ERR_UNSUPPORTED). */
+ * on `device` and bootstrap through memory instead of NCCL.  The kernel code, windows, peer
+ * stores and cross-rank barriers are the multi-GPU ones; each rank's gc_color_dist must be
+ * called concurrently from its own host thread.  The emulated ranks run in ONE cooperative
+ * launch (rank q on CTAs [qG, (q+1)G), issued by rank 0's thread), so that all of them are
+ * co-resident by construction. */
 gc_status gc_comm_init_local(gc_comm** comms_out, int32_t world, int32_t device);
 
 /*

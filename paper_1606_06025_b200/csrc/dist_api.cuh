@@ -59,6 +59,8 @@ struct LocalGroup {
   int arrived = 0;
   uint64_t gen = 0;
   std::vector<std::vector<uint8_t>> slot[2];
+  std::vector<Params> params;   // the ranks' kernel parameters of the shared launch
+  float kernel_ms = 0;
 };
 
 constexpr size_t kBootBytes = 256;  // largest bootstrap record
@@ -106,6 +108,7 @@ struct gc_comm {
   bool mapped[MAX_RANKS] = {};     // peer[q] is an IPC mapping to close
   uint32_t epoch = 0;              // cross-rank barrier epochs used so far (same on every rank)
   DevInfo* hinfo = nullptr;        // pinned: read back after a launch without a staging copy
+  void* dparams = nullptr;         // device Params of the launch this rank issues ([world] when emulating)
   bool broken = false;
 };
 
@@ -271,6 +274,7 @@ static gc_status comm_common(gc_comm* c, int32_t device) {
   }
   e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->hinfo, sizeof(DevInfo), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dparams, sizeof(Params) * MAX_RANKS);
   if (e == cudaSuccess && !c->lg) e = cudaMalloc(&c->boot, kBootBytes * (1 + MAX_RANKS));
   cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(e, "gc_comm: stream / bootstrap buffer");
@@ -316,21 +320,11 @@ gc_status gc_comm_init_local(gc_comm** comms_out, int32_t world, int32_t device)
     set_err("gc_comm_init_local: world must be 1..%d", MAX_RANKS);
     return GC_ERR_INVALID_ARGUMENT;
   }
-  {
-    // every rank's kernel must run concurrently on its own stream: streams beyond the device's
-    // hardware connections share queues and would serialise two ranks (deadlock)
-    const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
-    const int conn = e ? atoi(e) : 8;
-    if (world > 1 && 2 * world > conn) {
-      set_err("gc_comm_init_local: %d emulated ranks need CUDA_DEVICE_MAX_CONNECTIONS >= %d (set before CUDA "
-              "initialises; it is %d)", world, 2 * world, conn);
-      return GC_ERR_UNSUPPORTED;
-    }
-  }
   LocalGroup* g = new LocalGroup();
   g->world = world;
   g->slot[0].resize(world);
   g->slot[1].resize(world);
+  g->params.resize(world);
   for (int q = 0; q < world; ++q) comms_out[q] = nullptr;
   for (int q = 0; q < world; ++q) {
     gc_comm* c = new gc_comm();
@@ -358,6 +352,7 @@ gc_status gc_comm_destroy(gc_comm* c) {
   close_window(c);
   if (c->boot) cudaFree(c->boot);
   if (c->hinfo) cudaFreeHost(c->hinfo);
+  if (c->dparams) cudaFree(c->dparams);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->nccl && nccl_api()->CommDestroy) nccl_api()->CommDestroy(c->nccl);
   if (c->lg && --c->lg->refs == 0) delete c->lg;
@@ -594,10 +589,8 @@ gc_status gc_color_dist(gc_comm* c, int64_t n_global, int64_t v_begin, int64_t v
     void* fn = pick_persistent_dist(sbytes, (int)o.policy, cw, kn.variant == 1);
     int per_sm = 0;
     auto prepare_launch = [&]() -> gc_status {
-      // Everything that may need the context idle happens here, before the agreement below and
-      // so while no rank's kernel runs: module loading of the instance (lazy loading would
-      // load it at the first launch, and that load can wait for the other ranks' already
-      // spinning kernels: deadlock), occupancy, events; then DevInfo is zeroed.
+      // module loading of the instance, occupancy and events while no kernel runs; then this
+      // rank's DevInfo is zeroed (before any rank's kernel can write into it: agreed below)
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, fn));
       CK(occupancy(c->dev, fn, &per_sm));
@@ -609,46 +602,83 @@ gc_status gc_color_dist(gc_comm* c, int64_t n_global, int64_t v_begin, int64_t v
       CK(cudaStreamSynchronize(s));
       return GC_OK;
     };
-    // every rank's DevInfo is zeroed before any rank's kernel can write into it
     if ((st = agree(c, prepare_launch())) != GC_OK) return st;
+    if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
+    // One launch per GPU.  Emulated ranks (one GPU) share ONE cooperative launch of
+    // world x G CTAs, rank q taking CTAs [qG, (q+1)G): co-resident by construction.  (Separate
+    // concurrent cooperative launches per rank were measured on B200 to leave some CTAs of a
+    // rank's grid unscheduled while the other ranks' CTAs spin: a deadlock.)
+    const int ranks_in_launch = c->lg ? c->world : 1;
+    const int G = (f.sms * per_sm) / ranks_in_launch;
+    grid_used = G;
     p.st = c->win + L.st;
     p.epoch_base = c->epoch;
+    p.G = G;
+    p.blk0 = c->lg ? c->rank * G : 0;
+    p.nranks_in_launch = ranks_in_launch;
     cudaError_t e = cudaSuccess;
-    if (o.blocks_per_sm && (int)o.blocks_per_sm < per_sm) per_sm = (int)o.blocks_per_sm;
-    // one-process emulation: the ranks' kernels share this GPU and must all be resident; one CTA
-    // slot per SM is left free for the process's other work (copies, memsets, other threads)
-    int grid = c->lg ? (f.sms * (per_sm > 1 ? per_sm - 1 : 1)) / c->world : f.sms * per_sm;
-    if (grid < 1) grid = 1;
-    grid_used = grid;
-    if (ev0 && attempt == 0) cudaEventRecord(ev0, s);
-    // From the launch until this rank's kernel ends, the host thread only waits on the stream:
-    // a pageable copy here (staging-buffer setup) was observed to stall the other emulated ranks'
-    // launches behind the spinning kernels.  The read-back goes to pinned memory.
-    void* args[] = {&p};
-    e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(c->hinfo, p.info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) memcpy(&hinfo, c->hinfo, sizeof(DevInfo));
-    if (e != cudaSuccess) {
-      c->broken = true;  // the other ranks may be waiting in a barrier of this launch
-      return cuda_fail(e, "gc_color_dist: persistent kernel");
+    if (c->lg) c->lg->params[c->rank] = p;
+    if ((st = agree(c, GC_OK)) != GC_OK) return st;  // every rank's Params are in place
+    if (!c->lg || c->rank == 0) {
+      const Params* src = c->lg ? c->lg->params.data() : &p;
+      e = cudaMemcpyAsync(c->dparams, src, sizeof(Params) * ranks_in_launch, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess && ev0 && attempt == 0) e = cudaEventRecord(ev0, s);
+      const Params* dpp = (const Params*)c->dparams;
+      void* args[] = {&dpp};
+      if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3(G * ranks_in_launch), dim3(BLOCK), args, 0, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        c->broken = true;  // the other ranks may be waiting in a barrier of this launch
+        cuda_fail(e, "gc_color_dist: persistent kernel");
+      }
     }
+    if (c->lg) {  // the emulated ranks learn that the shared launch ended (or failed)
+      gc_status launched = e == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+      if ((st = agree(c, launched)) != GC_OK) {
+        c->broken = true;
+        return st;
+      }
+    } else if (e != cudaSuccess) {
+      return GC_ERR_CUDA;
+    }
+    e = cudaMemcpyAsync(c->hinfo, p.info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      c->broken = true;
+      return cuda_fail(e, "gc_color_dist: read-back");
+    }
+    memcpy(&hinfo, c->hinfo, sizeof(DevInfo));
     c->epoch += hinfo.bar_gen;  // every rank passed the same barriers
     sbytes_used = sbytes;
     if (hinfo.status == ST_NEED16 && sbytes < 2) sbytes = 2;
     else if (hinfo.status == ST_NEED32 && sbytes < 4) sbytes = 4;
     else break;
   }
-  if (ev1) {
-    cudaEventRecord(ev1, s);
-    cudaEventSynchronize(ev1);
-    cudaEventElapsedTime(o.kernel_ms, ev0, ev1);
+  if (ev1) {  // (emulated ranks other than 0 launched nothing: they report rank 0's time)
+    if (!c->lg || c->rank == 0) {
+      cudaEventRecord(ev1, s);
+      cudaEventSynchronize(ev1);
+      cudaEventElapsedTime(o.kernel_ms, ev0, ev1);
+      if (c->lg) c->lg->kernel_ms = *o.kernel_ms;
+    }
+    if (c->lg) {
+      agree(c, GC_OK);
+      *o.kernel_ms = c->lg->kernel_ms;
+    }
   }
   if (hinfo.status == ST_WATCHDOG) {
     c->broken = true;
+    {
+      char buf[512];
+      int o = 0;
+      for (int b = 0; b < grid_used && b < 1024 && o < 400; ++b)
+        if ((hinfo.stage[b] >> 20) != 1u || b == 0)
+          o += snprintf(buf + o, sizeof(buf) - o, " cta%d:%x", b, hinfo.stage[b]);
+      fprintf(stderr, "gc_color_dist watchdog rank %d stages:%s\n", c->rank, buf);
+    }
     set_err("gc_color_dist: device watchdog fired (cross-rank barrier timeout; rank %d: waiting for rank %d "
-            "at epoch %u, %u of %d local CTAs arrived)", c->rank, (int)hinfo.diag[0] - 1, hinfo.diag[1], hinfo.diag[2],
-            (int)grid_used);
+            "at epoch %u, %u of %d local CTAs arrived, %u started; status word %u)", c->rank, (int)hinfo.diag[0] - 1,
+            hinfo.diag[1], hinfo.diag[2], (int)grid_used, hinfo.diag[3], hinfo.status);
     return GC_ERR_CUDA;
   }
   if (hinfo.status == ST_NO_CONVERGENCE) {

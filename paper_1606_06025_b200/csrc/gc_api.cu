@@ -224,6 +224,19 @@ bool resolve_knobs(const gc_tuning* t, Knobs* k) {
   return true;
 }
 
+// Kernel-variant hints per graph (device, row_ptr address, n, m), a small direct-mapped cache.
+struct HintEntry { int dev; const void* rp; int64_t n, m; int variant; };
+HintEntry g_hint[64];
+int variant_hint(int dev, const void* rp, int64_t n, int64_t m) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  const HintEntry& h = g_hint[((uintptr_t)rp >> 8 ^ (uint64_t)n) % 64];
+  return (h.rp == rp && h.dev == dev && h.n == n && h.m == m) ? h.variant : -1;
+}
+void set_variant_hint(int dev, const void* rp, int64_t n, int64_t m, int variant) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_hint[((uintptr_t)rp >> 8 ^ (uint64_t)n) % 64] = HintEntry{dev, rp, n, m, variant};
+}
+
 const char* val_err_name(uint32_t code) {
   switch (code) {
     case VE_ROWPTR: return "row_ptr[0] != 0 or row_ptr decreasing";
@@ -517,6 +530,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     ~EvGuard() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
   } evg{ev0, ev1};
   int sbytes = 4, sbytes_used = 4;
+  bool fat_cand_for_hint = false;
   if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
     // ---- persistent cooperative kernel: the whole run in one launch
     if (!prop.coop) {
@@ -526,19 +540,13 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     // 8-bit state words first; a colour > 127 makes the kernel stop at the next barrier with
     // ST_NEED16 and a vertex of degree > 32766 stops it in its prologue with ST_NEED32; the
     // run is then repeated with the wider words (at most two restarts).
-    // kernel variant: bounded degree (<= 64) and >= 8 entries per row -> 3 CTAs/SM (sgr_kernels.cuh)
-    bool fat = false;
-    if (kn.variant < 0 && push && n1 && m >= 8 * n) {
-      void* dmax;
-      CK(sc.alloc(&dmax, sizeof(uint32_t)));
-      CK(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
-      k_maxdeg<<<prop.sms * 8, BLOCK, 0, s>>>((int32_t)n, d_rp, (uint32_t*)dmax);
-      CK(cudaGetLastError());
-      uint32_t mx = 0;
-      CK(cudaMemcpyAsync(&mx, dmax, sizeof(mx), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      fat = mx <= 64;
-    }
+    // kernel variant: bounded degree (<= 64) and >= 8 entries per row -> 3 CTAs/SM (sgr_kernels.cuh).
+    // The max degree is known only after the ingest, so the choice for a graph is remembered
+    // from its previous call (variant_hint; the first call runs the default variant).  A stale
+    // hint can only cost speed: every variant computes the same colouring.
+    const bool fat_candidate = push && n1 && m >= 8 * n;
+    fat_cand_for_hint = fat_candidate;
+    bool fat = fat_candidate && variant_hint(dev, d_rp, n, m) == 1;
     if (kn.variant >= 0) fat = kn.variant == 1;
     sbytes = kn.state_bytes;
     for (int attempt = 0; attempt < 3; ++attempt) {
@@ -628,6 +636,10 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
 
   DevInfo hinfo;
   CK(cudaMemcpyAsync(&hinfo, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+  if (!(o.flags & GC_FLAG_HOST_ROUNDS)) {
+    CK(cudaStreamSynchronize(s));
+    set_variant_hint(dev, d_rp, n, m, fat_cand_for_hint && hinfo.maxdeg <= 64u ? 1 : 0);
+  }
   if (!out_dev) CK(cudaMemcpyAsync(colors_out, dcol, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (ev1) CK(cudaEventElapsedTime(o.kernel_ms, ev0, ev1));

@@ -8,7 +8,7 @@
 using namespace gcdev_dist;
 
 void* gc_inst_dist_u16(int pol, bool cw) {
-  if (pol == HIGHER_ID) return cw ? (void*)sgr_persistent<uint16_t, HIGHER_ID, true, true> : (void*)sgr_persistent<uint16_t, HIGHER_ID, true, false>;
-  if (pol == LOWER_ID) return cw ? (void*)sgr_persistent<uint16_t, LOWER_ID, true, true> : (void*)sgr_persistent<uint16_t, LOWER_ID, true, false>;
-  return cw ? (void*)sgr_persistent<uint16_t, DEGREE, true, true> : (void*)sgr_persistent<uint16_t, DEGREE, true, false>;
+  if (pol == HIGHER_ID) return cw ? (void*)sgr_dist<uint16_t, HIGHER_ID, true> : (void*)sgr_dist<uint16_t, HIGHER_ID, false>;
+  if (pol == LOWER_ID) return cw ? (void*)sgr_dist<uint16_t, LOWER_ID, true> : (void*)sgr_dist<uint16_t, LOWER_ID, false>;
+  return cw ? (void*)sgr_dist<uint16_t, DEGREE, true> : (void*)sgr_dist<uint16_t, DEGREE, false>;
 }

@@ -8,13 +8,13 @@
 using namespace gcdev_dist;
 
 void* gc_inst_dist_u8(int pol, bool cw) {
-  if (pol == HIGHER_ID) return cw ? (void*)sgr_persistent<uint8_t, HIGHER_ID, true, true> : (void*)sgr_persistent<uint8_t, HIGHER_ID, true, false>;
-  if (pol == LOWER_ID) return cw ? (void*)sgr_persistent<uint8_t, LOWER_ID, true, true> : (void*)sgr_persistent<uint8_t, LOWER_ID, true, false>;
-  return cw ? (void*)sgr_persistent<uint8_t, DEGREE, true, true> : (void*)sgr_persistent<uint8_t, DEGREE, true, false>;
+  if (pol == HIGHER_ID) return cw ? (void*)sgr_dist<uint8_t, HIGHER_ID, true> : (void*)sgr_dist<uint8_t, HIGHER_ID, false>;
+  if (pol == LOWER_ID) return cw ? (void*)sgr_dist<uint8_t, LOWER_ID, true> : (void*)sgr_dist<uint8_t, LOWER_ID, false>;
+  return cw ? (void*)sgr_dist<uint8_t, DEGREE, true> : (void*)sgr_dist<uint8_t, DEGREE, false>;
 }
 
 void* gc_inst_dist_fat(int pol, bool cw) {
-  if (pol == HIGHER_ID) return cw ? (void*)sgr_persistent_fat<HIGHER_ID, true> : (void*)sgr_persistent_fat<HIGHER_ID, false>;
-  if (pol == LOWER_ID) return cw ? (void*)sgr_persistent_fat<LOWER_ID, true> : (void*)sgr_persistent_fat<LOWER_ID, false>;
-  return cw ? (void*)sgr_persistent_fat<DEGREE, true> : (void*)sgr_persistent_fat<DEGREE, false>;
+  if (pol == HIGHER_ID) return cw ? (void*)sgr_dist_fat<HIGHER_ID, true> : (void*)sgr_dist_fat<HIGHER_ID, false>;
+  if (pol == LOWER_ID) return cw ? (void*)sgr_dist_fat<LOWER_ID, true> : (void*)sgr_dist_fat<LOWER_ID, false>;
+  return cw ? (void*)sgr_dist_fat<DEGREE, true> : (void*)sgr_dist_fat<DEGREE, false>;
 }

@@ -105,12 +105,14 @@ struct DevInfo {
   unsigned long long bad;       // validation / verify: ~(smallest offending key), 0 = none
   uint32_t err_code;
   uint32_t gtot[3];             // multi-GPU: global |W| by round (r % 3), summed by the ranks' barrier leaders
+  uint32_t decision;            // status agreed by the last barrier (published with its generation flip)
   uint32_t diag[4];             // watchdog diagnostics: [0] 1 + rank not heard from, [1] epoch, [2] arrivals seen
-  uint32_t pad2[24];
+  uint32_t pad2[23];
   uint32_t bar_count;           // grid barrier (own 128-B lines)
   uint32_t pad3[31];
   uint32_t bar_gen;
   uint32_t pad4[31];
+  uint32_t stage[1024];         // multi-GPU debug: per local CTA, the last step reached (watchdog report)
 };
 
 // Worklist entry: the vertex, the split k = number of its neighbours with a lower id
@@ -179,12 +181,20 @@ struct Params {
   int32_t n_global;
   uint32_t epoch_base;          // cross-rank barrier epochs already used by earlier launches
   int32_t rb[MAX_RANKS + 1];    // rank q owns [rb[q], rb[q+1]); entries past nranks = INT32_MAX
+  int32_t G, blk0;              // multi-GPU kernels: this rank's CTAs are [blk0, blk0 + G) of the launch
+  int32_t nranks_in_launch;     //   ... and the launch holds nranks_in_launch ranks (1 on real GPUs)
+  int32_t pad_;
   uint8_t* bmask;               // global-indexed: bit q set when rank q holds local vertex v as a ghost
   const Peer* peer;             // [nranks] in device memory (indexed by rank at run time; a table in
                                 //   the kernel parameters would be copied to the stack)
 };
 
 __device__ __forceinline__ bool dist(const Params& p) { return kDist && p.nranks > 1; }
+// This rank's CTAs: the whole grid on one GPU; in a multi-GPU kernel launch the CTAs
+// [blk0, blk0 + G) (one rank per launch on real GPUs; every emulated rank of a one-GPU test
+// group in one cooperative launch, so that all of them are co-resident by construction).
+__device__ __forceinline__ uint32_t nblk(const Params& p) { return kDist ? (uint32_t)p.G : gridDim.x; }
+__device__ __forceinline__ uint32_t blk(const Params& p) { return kDist ? blockIdx.x - (uint32_t)p.blk0 : blockIdx.x; }
 // Rank owning global vertex w (ranges are contiguous and ordered by rank).
 __device__ __forceinline__ int owner(const Params& p, int32_t w) {
   int q = 0;
@@ -338,13 +348,10 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 // ---------------------------------------------------------------- multi-GPU propagation
-// Run status (restart / no convergence / watchdog): every rank must stop at the same barrier,
-// so a status is written into every rank's DevInfo before the barrier that reads it.
+// Run status (restart / no convergence): raised during a phase, acted on by every CTA of every
+// rank at the barrier that ends the phase (grid_sync).
 __device__ __forceinline__ void set_status(const Params& p, uint32_t s) {
-  atomicExch(&p.info->status, s);
-  if (dist(p))
-    for (int q = 0; q < p.nranks; ++q)
-      if (q != p.rank) atomicExch(&p.peer[q].info->status, s);
+  atomicMax(&p.info->status, s);  // the barrier ending the phase carries it to every rank
 }
 // A local vertex's new state word goes to the replicas of the ranks that hold it as a ghost
 // (the owners of its neighbours): the device-initiated exchange of SURVEY N2.
@@ -377,15 +384,23 @@ __device__ __forceinline__ void bcast_word(const Params& p, int32_t v, uint32_t 
 // release-stores the epoch into its slot of every rank's flag array and acquire-polls its own
 // flags until every rank has signalled the epoch, and only then flips the local generation.
 // Epochs continue across launches (p.epoch_base), so the flags are never reset.
-static __device__ __noinline__ void xrank_sync(const Params& p, uint32_t gen, int nxt) {
+// The barrier also decides, once per rank, whether the run goes on: the last CTA to arrive
+// reads the rank's status word (written before the arrivals it has observed), multi-GPU ranks
+// exchange it with the epoch (slot [q][1] written before the release of slot [q][0]) and take
+// the maximum, and the decision is published with the generation flip.  Every CTA of every rank
+// therefore leaves the run at the same barrier (a status raised during a phase, e.g. the 8-bit
+// state-word overflow, stops everybody at the barrier that ends that phase).
+static __device__ __noinline__ uint32_t xrank_sync(const Params& p, uint32_t gen, int nxt, uint32_t st) {
   if (nxt >= 0) {
     uint32_t t = 0;
 #pragma unroll
     for (int b = 0; b < NBIN; ++b) t += ld_relaxed(&p.info->cnt[nxt][b]);
     for (int q = 0; q < p.nranks; ++q) atomicAdd(&p.peer[q].info->gtot[nxt], t);
   }
-  __threadfence_system();
   const uint32_t ep = p.epoch_base + gen;
+  // status slot by epoch parity: a rank one barrier ahead writes the other slot
+  for (int q = 0; q < p.nranks; ++q) p.peer[q].xflag[32 * p.rank + 1 + (ep & 1)] = st;
+  __threadfence_system();
   for (int q = 0; q < p.nranks; ++q) st_release_sys(p.peer[q].xflag + 32 * p.rank, ep);
   const unsigned long long t0 = globaltimer();
   const uint32_t* mine = p.peer[p.rank].xflag;
@@ -395,23 +410,36 @@ static __device__ __noinline__ void xrank_sync(const Params& p, uint32_t gen, in
       if (globaltimer() - t0 > p.timeout_ns) {
         p.info->diag[0] = 1u + (uint32_t)q;
         p.info->diag[1] = ep;
-        atomicExch(&p.info->status, (uint32_t)ST_WATCHDOG);
-        return;
+        return ST_WATCHDOG;
       }
     }
+    // (a rank can be at most one barrier ahead: ep + 1 needs this rank's ep + 1)
+    const uint32_t sq = *(volatile const uint32_t*)(mine + 32 * q + 1 + (ep & 1));
+    st = sq > st ? sq : st;
   }
+  return st;
 }
 
 static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
+  __shared__ uint32_t s_go;
   __syncthreads();
   if (threadIdx.x == 0) {
     DevInfo* I = p.info;
+    if (kDist) I->stage[blk(p) & 1023] = 0x100000u | (ld_relaxed(&I->bar_gen) & 0xfffffu);
     const uint32_t gen = ld_relaxed(&I->bar_gen);
     if (dist(p)) __threadfence_system();
     else __threadfence();
     const uint32_t arrived = atomicAdd(&I->bar_count, 1u);
-    if (arrived == gridDim.x - 1) {
-      if (dist(p)) xrank_sync(p, gen + 1, nxt);
+    uint32_t go = 1;
+    if (arrived == nblk(p) - 1) {
+      __threadfence();  // the arrivals' status writes are ordered before this read
+      uint32_t st = ld_relaxed(&I->status);
+      if (dist(p)) {
+        st = xrank_sync(p, gen + 1, nxt, st);
+        if (st != ST_OK) atomicMax(&I->status, st);  // the host reads the agreed status
+      }
+      I->decision = st;
+      go = st == ST_OK;
       atomicExch(&I->bar_count, 0u);
       st_release(&I->bar_gen, gen + 1);
     } else {
@@ -421,14 +449,17 @@ static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
         if (globaltimer() - t0 > p.timeout_ns) {
           I->diag[2] = ld_relaxed(&I->bar_count);
           atomicExch(&I->status, (uint32_t)ST_WATCHDOG);
+          go = 0;
           break;
         }
       }
+      __threadfence();  // acquire side: orders the decision and the next phase's reads after the flip
+      if (go) go = ld_relaxed(&I->decision) == ST_OK;
     }
-    __threadfence();  // acquire side: orders the next phase's reads after the flip
+    s_go = go;
   }
   __syncthreads();
-  return ld_relaxed(&p.info->status) == ST_OK;
+  return s_go != 0;
 }
 
 // ---------------------------------------------------------------- bins

@@ -22,14 +22,14 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
   __syncthreads();
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * BLOCK;
+  const int64_t stride = (int64_t)nblk(p) * BLOCK;
   bool wide = false;
   uint32_t maxdeg = 0;
   // the row offsets of the next iteration's vertex are loaded one iteration ahead, so that
   // their latency overlaps this vertex's split search
-  const int64_t first = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31) + lane;
+  const int64_t first = (int64_t)blk(p) * BLOCK + (threadIdx.x & ~31) + lane;
   int64_t nbeg = first < p.n ? ldr(p.rp, first) : 0, nend = first < p.n ? ldr(p.rp, first + 1) : 0;
-  for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
+  for (int64_t base = (int64_t)blk(p) * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
     int b = -1;
@@ -83,7 +83,7 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
     if (dist(p)) for (int q = 0; q < p.nranks; ++q) atomicMax(&p.peer[q].info->maxdeg, maxdeg);
     else atomicMax(&p.info->maxdeg, maxdeg);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blk(p) == 0 && threadIdx.x == 0) {
     p.info->wlp[0] = (unsigned long long)p.wl0;
     p.info->wlp[1] = (unsigned long long)p.wl1;
   }
@@ -96,10 +96,10 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
 // neighbour of v — exactly the ranks that read v's state word (the graph is symmetric), so the
 // only ones its tentative colours and commit are sent to.  One warp per local vertex.
 __device__ __forceinline__ void prologue_dist(const Params& p) {
-  const int64_t T = (int64_t)gridDim.x * BLOCK;
+  const int64_t T = (int64_t)nblk(p) * BLOCK;
   const int lane = threadIdx.x & 31;
   const int64_t nw = T >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5; u < p.n; u += nw) {
+  for (int64_t u = ((int64_t)blk(p) * BLOCK + threadIdx.x) >> 5; u < p.n; u += nw) {
     const int64_t beg = ldr(p.rp, u), end = ldr(p.rp, u + 1);
     uint32_t m = 0;
     for (int64_t e = beg + lane; e < end; e += 32) {
@@ -109,12 +109,12 @@ __device__ __forceinline__ void prologue_dist(const Params& p) {
     m = __reduce_or_sync(FULL, m);
     if (lane == 0) sts(p.bmask + p.v_base + u, m);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.info->gtot[1] = (uint32_t)p.n_global;
+  if (blk(p) == 0 && threadIdx.x == 0) p.info->gtot[1] = (uint32_t)p.n_global;
 }
 template <class S>
 __device__ __forceinline__ void fill_replica(const Params& p) {
   S* st = (S*)p.st;
-  for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < p.n_global; v += (int64_t)gridDim.x * BLOCK)
+  for (int64_t v = (int64_t)blk(p) * BLOCK + threadIdx.x; v < p.n_global; v += (int64_t)nblk(p) * BLOCK)
     sts(st + v, 1u);
 }
 
@@ -122,8 +122,8 @@ __device__ __forceinline__ void fill_replica(const Params& p) {
 // bin is free, reading C12).
 __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bins) {
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * BLOCK;
-  for (int64_t base = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
+  const int64_t stride = (int64_t)nblk(p) * BLOCK;
+  for (int64_t base = (int64_t)blk(p) * BLOCK + (threadIdx.x & ~31); base < p.n; base += stride) {
     const int64_t v = base + lane;
     const bool act = v < p.n;
     int b = -1;
@@ -145,7 +145,7 @@ __device__ __forceinline__ void prologue_scatter(const Params& p, const Bins& bi
       if (b == k) stw(p.wl0 + bins.off[k] + pos + __popc(m & lanemask_lt()), e);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = p.info->binsize[threadIdx.x];
+  if (blk(p) == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = p.info->binsize[threadIdx.x];
 }
 
 // ---- warp-flattened segment loops
@@ -297,7 +297,7 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, uint32_t r, const 
                                              const uint32_t* nb, bool mark, Work& wk) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
-  const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
+  const uint32_t gw = blk(p) * WARPS + (threadIdx.x >> 5), nw = nblk(p) * WARPS;
   uint32_t nchg = 0;
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) {
@@ -341,7 +341,7 @@ __device__ __forceinline__ void zero_plane(const Params& p, uint32_t r) {
   uint4* q = (uint4*)(p.fmp + (int64_t)(r / 8) * p.plane);
   const int64_t nq = p.plane / 16;
   const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < nq; i += (int64_t)gridDim.x * BLOCK) q[i] = z;
+  for (int64_t i = (int64_t)blk(p) * BLOCK + threadIdx.x; i < nq; i += (int64_t)nblk(p) * BLOCK) q[i] = z;
 }
 
 // Pull mode (GC_FLAG_PULL_FIRSTFIT, the paper's FirstFit): full neighbour scan per round;
@@ -351,7 +351,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
                                              Work& wk, uint32_t* s_win) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
-  const uint32_t gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
+  const uint32_t gw = blk(p) * WARPS + (threadIdx.x >> 5), nw = nblk(p) * WARPS;
   {
     const WE* Wb = W + bins.off[0];
     for (uint32_t base = gw * 32; base < nb[0]; base += nw * 32) {
@@ -376,7 +376,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
   }
   {
     const WE* Wb = W + bins.off[1];
-    for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
+    for (uint32_t i = blk(p); i < nb[1]; i += nblk(p)) {
       const int32_t v = ldw_v(Wb + i);
       const uint32_t t = firstfit_cta<S, CW>(p, v, 1u, wk, s_win);
       if (threadIdx.x == 0) store_tent<S>(p, st, v, t);
@@ -387,7 +387,7 @@ __device__ __forceinline__ void phase_a_pull(const Params& p, const Bins& bins, 
 // reset the counters round r+1 will push into and the work queues it will pop from
 // (last used in round r-2)
 __device__ __forceinline__ void reset_next(const Params& p, uint32_t r) {
-  if (blockIdx.x == 0 && threadIdx.x < NBIN) {
+  if (blk(p) == 0 && threadIdx.x < NBIN) {
     p.info->cnt[(r + 1) % 3][threadIdx.x] = 0;
     p.info->qctr[(r + 1) % 3][threadIdx.x][0] = 0;
     if (threadIdx.x == 0) {
@@ -409,7 +409,7 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
   reset_next(p, r);
-  if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
+  if (CW && threadIdx.x == 0 && blk(p) == 0) {
     wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
     wk.v[W_SA_ENT] += (unsigned long long)nb[0] + nb[1];
   }
@@ -439,18 +439,18 @@ template <class S, int POL, bool CW>
 __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool mark, Work& wk) {
   S* st = (S*)p.st;
   reset_next(p, r);
-  if (CW && threadIdx.x == 0 && blockIdx.x == 0) {
+  if (CW && threadIdx.x == 0 && blk(p) == 0) {
     const uint32_t cur = r % 3;
     wk.v[W_A_VERT] += (unsigned long long)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
     wk.v[W_DA_SWEEP] += (unsigned long long)p.n;
   }
   zero_plane(p, r);
   const int lane = threadIdx.x & 31;
-  const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
+  const int64_t nthreads = (int64_t)nblk(p) * BLOCK;
   // groups of 16 global ids aligned to 16 covering this rank's range [vlo, vend)
   const int64_t vlo = p.v_base, vend = (int64_t)p.v_base + p.n, lo16 = vlo & ~(int64_t)15;
   const int64_t ngroups = (vend - lo16 + 15) / 16;
-  const int64_t g0 = (int64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31);
+  const int64_t g0 = (int64_t)blk(p) * BLOCK + (threadIdx.x & ~31);
   uint32_t nchg = 0;
   int32_t* clist = bsmem().clist[threadIdx.x >> 5];
   for (int64_t gb = g0; gb < ngroups; gb += nthreads) {
@@ -761,7 +761,7 @@ __device__ __forceinline__ void phase_b_coop(const Params& p, const WE* Wb, uint
                                              bool mark, Work& wk, int* s_first, uint32_t rec_round) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t nwarps = nblk(p) * WARPS;
   const uint32_t ch = max(1u, min(64u, cnt / (4u * nwarps)));
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < cnt; c0 = pop_chunk(q, ch, lane)) {
     const uint32_t cend = min(c0 + ch, cnt);
@@ -840,7 +840,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
 #pragma unroll
   for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blk(p) == 0 && threadIdx.x == 0) {
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1];
     if (CW) {
       wk.v[W_B_VERT] += (unsigned long long)nb[0] + nb[1];
@@ -856,7 +856,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   {
     const WE* Wb = W + bins.off[1];
     WE* Ob = Wout + bins.off[1];
-    for (uint32_t i = blockIdx.x; i < nb[1]; i += gridDim.x) {
+    for (uint32_t i = blk(p); i < nb[1]; i += nblk(p)) {
       WE e = ldw(Wb + i);
       if (threadIdx.x == 0) {  // one read of the state word and the dirty mark, broadcast
         uint32_t x = lds(st + e.v) & SW<S>::CMASK;
@@ -1223,7 +1223,7 @@ __device__ __forceinline__ void phase_a_list(const Params& p, uint32_t r, Work& 
   const uint32_t nwin = ld_relaxed(&p.info->wl_cnt[(r - 1) % 3]);
   const int32_t* WL = ((r - 1) & 1) ? p.wlw1 : p.wlw0;
   uint32_t* q = &p.info->qctr[r % 3][1][0];
-  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t nwarps = nblk(p) * WARPS;
   const uint32_t ch = max(1u, min(32u, nwin / (4u * nwarps)));
   uint32_t nchg = 0;
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nwin; c0 = pop_chunk(q, ch, lane)) {
@@ -1284,13 +1284,13 @@ template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void phase_b_list(const Params& p, uint32_t r, uint32_t tot, Work& wk) {
   S* st = (S*)p.st;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blk(p) == 0 && threadIdx.x == 0) {
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
     if (CW) wk.v[W_B_VERT] += tot;
   }
   const uint32_t nd = ld_relaxed(&p.info->dl_cnt[r % 3]);
   uint32_t* q = &p.info->qctr[r % 3][0][0];
-  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t nwarps = nblk(p) * WARPS;
   const uint32_t ch = max(1u, min(64u, nd / (4u * nwarps)));
   int* s_first = bsmem().cwfirst[warp];
   for (uint32_t c0 = pop_chunk(q, ch, lane); c0 < nd; c0 = pop_chunk(q, ch, lane)) {
@@ -1330,7 +1330,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   S* st = (S*)p.st;
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blk(p) == 0 && threadIdx.x == 0) {
     const uint32_t tot = ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
     if (CW) {
@@ -1344,7 +1344,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   {
     const uint32_t nh = bins.size[1];
     WE* Ob = Wout + bins.off[1];
-    for (uint32_t i = blockIdx.x; i < nh; i += gridDim.x) {
+    for (uint32_t i = blk(p); i < nh; i += nblk(p)) {
       WE e = ldw(p.heavy + i);
       if (threadIdx.x == 0) {  // one read of the state word and the dirty mark, broadcast
         uint32_t x = lds(st + e.v);
@@ -1372,7 +1372,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       __syncthreads();
     }
   }
-  const uint32_t nwarps = gridDim.x * WARPS;
+  const uint32_t nwarps = nblk(p) * WARPS;
   // chunk offsets c count from lo16 (this rank's first id rounded down to 16): vertex lo16 + c
   const uint32_t vlo = (uint32_t)p.v_base, vend = vlo + (uint32_t)p.n, lo16 = vlo & ~15u;
   const uint32_t nv = vend - lo16;
@@ -1477,8 +1477,8 @@ template <class S>
 __device__ __forceinline__ void epilogue(const Params& p) {
   const S* st = (const S*)p.st;
   uint32_t mx = 0;
-  const int64_t stride = (int64_t)gridDim.x * BLOCK;
-  for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < p.n; v += stride) {
+  const int64_t stride = (int64_t)nblk(p) * BLOCK;
+  for (int64_t v = (int64_t)blk(p) * BLOCK + threadIdx.x; v < p.n; v += stride) {
     const uint32_t c = lds(st + p.v_base + v) & SW<S>::CMASK;
     p.colors_out[v] = c;
     mx = c > mx ? c : mx;
@@ -1513,9 +1513,15 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   Work wk;
   wk.zero();
   const bool dense0 = PUSH && p.dense_div != 0;
+  if (kDist && threadIdx.x == 0) {
+    atomicAdd(&p.info->diag[3], 1u);  // CTAs started (watchdog report)
+    p.info->stage[blk(p) & 1023] = 1;
+  }
   if (dist(p)) {  // multi-GPU: replica fill + ghost masks (one cross-rank barrier)
     fill_replica<S>(p);
+    if (threadIdx.x == 0) p.info->stage[blk(p) & 1023] = 2;
     prologue_dist(p);
+    if (threadIdx.x == 0) p.info->stage[blk(p) & 1023] = 3;
     if (!grid_sync(p)) return;
   }
   prologue_count<S, POL, PUSH>(p, dense0);
@@ -1523,9 +1529,9 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   Bins bins;
   bins.load(p);
   if (!dense0) prologue_scatter(p, bins);
-  else if (blockIdx.x == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = bins.size[threadIdx.x];
+  else if (blk(p) == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = bins.size[threadIdx.x];
   if (!grid_sync(p)) return;
-  const bool stamp = p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool stamp = p.phase_ns && blk(p) == 0 && threadIdx.x == 0;
   if (stamp) p.phase_ns[0] = globaltimer();
 
   // The worklist pointers are re-read from DevInfo every round instead of being swapped in
@@ -1576,7 +1582,7 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
       phase_b<S, POL, PUSH, CW>(p, r, bins, Win, Wout, mark, wk, list_next);
     }
     // multi-GPU: |W_r| of the trace is the global one (the phase wrote the local count)
-    if (dist(p) && blockIdx.x == 0 && threadIdx.x == 0 && p.trace && r <= p.trace_cap)
+    if (dist(p) && blk(p) == 0 && threadIdx.x == 0 && p.trace && r <= p.trace_cap)
       p.trace[r - 1] = ld_relaxed(&p.info->gtot[cur]);
     if (!grid_sync(p, dist(p) ? (int)((r + 1) % 3) : -1)) return;
     if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
@@ -1590,7 +1596,7 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
     }
     if (left == 0) break;
     if (r >= p.max_rounds) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&p.info->status, (uint32_t)ST_NO_CONVERGENCE);  // same r on every rank
+      if (blk(p) == 0 && threadIdx.x == 0) atomicExch(&p.info->status, (uint32_t)ST_NO_CONVERGENCE);  // same r on every rank
       flush_work<CW>(p, wk);
       return;
     }
@@ -1598,7 +1604,7 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   }
   epilogue<S>(p);
   flush_work<CW>(p, wk);
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.info->rounds = r;
+  if (blk(p) == 0 && threadIdx.x == 0) p.info->rounds = r;
   if (dist(p)) grid_sync(p);  // every rank's num_colors holds the global max before the host reads it
 }
 
@@ -1614,18 +1620,31 @@ __global__ void __launch_bounds__(BLOCK, 3) sgr_persistent_fat(Params p) {
   sgr_body<uint8_t, POL, true, CW>(p);
 }
 
-#ifndef GC_INST_TU  // the non-template kernels below live in gc_api.cu only
-// Max degree (host-side kernel selection).
-__global__ void __launch_bounds__(BLOCK) k_maxdeg(int32_t n, const int64_t* __restrict__ rp, uint32_t* out) {
-  uint32_t mx = 0;
-  for (int64_t v = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v < n; v += (int64_t)gridDim.x * BLOCK) {
-    const int64_t d = __ldg(rp + v + 1) - __ldg(rp + v);
-    mx = max(mx, (uint32_t)min(d, (int64_t)0xffffffff));
-  }
-  mx = __reduce_max_sync(FULL, mx);
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+#ifdef GC_DIST_TU
+// Multi-GPU entry: `ranks` ranks' parameter blocks in device memory; the launch holds G =
+// gridDim.x / ranks CTAs per rank (one rank per launch on real GPUs; all emulated ranks of a
+// one-GPU test group in one cooperative launch).  A CTA copies its rank's Params into shared
+// memory (a run-time index into kernel parameters would put the whole block on the stack).
+__device__ __forceinline__ const Params& stage_params(const Params* __restrict__ pp) {
+  __shared__ __align__(16) Params sp;
+  const uint32_t G = gridDim.x / (uint32_t)pp[0].nranks_in_launch;
+  const Params* src = pp + blockIdx.x / G;
+  for (uint32_t i = threadIdx.x; i < sizeof(Params) / 4; i += BLOCK)
+    ((uint32_t*)&sp)[i] = ((const uint32_t*)src)[i];
+  __syncthreads();
+  return sp;
 }
+template <class S, int POL, bool CW>
+__global__ void __launch_bounds__(BLOCK, GC_MINB) sgr_dist(const Params* __restrict__ pp) {
+  sgr_body<S, POL, true, CW>(stage_params(pp));
+}
+template <int POL, bool CW>
+__global__ void __launch_bounds__(BLOCK, 3) sgr_dist_fat(const Params* __restrict__ pp) {
+  sgr_body<uint8_t, POL, true, CW>(stage_params(pp));
+}
+#endif
 
+#ifndef GC_INST_TU  // the non-template kernels below live in gc_api.cu only
 // ---------------------------------------------------------------- host-driven ablation
 // GC_FLAG_HOST_ROUNDS: the same phases (32-bit state words), one non-cooperative launch
 // each, the host reading |W_{r+1}| after every round ("CPU ... controlling the progress").

@@ -204,9 +204,12 @@ def color_partitioned_local(row_ptr, col_idx, bounds, policy: str = "higher_id",
     if own:
         for c in comms:
             c.close()
-    for ex in errors:
-        if ex is not None:
-            raise ex
+    bad = [(q, ex) for q, ex in enumerate(errors) if ex is not None]
+    if bad:
+        q0, ex0 = bad[0]
+        if len(bad) > 1:  # every rank's error (the first is often a consequence of another's)
+            ex0.args = (ex0.args[0] + " | " + " | ".join(f"rank {q}: {ex}" for q, ex in bad[1:]),)
+        raise ex0
     parts = []
     for r in results:
         c = r.colors

@@ -7,8 +7,6 @@ colours equal one-GPU gc_color's.
 import os
 import sys
 
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # emulated ranks: one hardware queue each
-os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

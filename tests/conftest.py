@@ -3,15 +3,6 @@ import sys
 
 import pytest
 
-# The one-process emulation of the multi-GPU path (tests/test_dist.py) runs up to 8 ranks'
-# persistent kernels concurrently on 8 streams; with the default 8 hardware connections two of
-# them can share a queue and serialise (the second never starts while the first waits for it).
-# Read by CUDA at context creation, so set before torch initialises CUDA.
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-# ... and a rank's first launch of a kernel instance must not lazily load the module while the
-# other ranks' kernels spin (the library also loads each instance before the ranks launch).
-os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
-
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -1,0 +1,30 @@
+"""compute-sanitizer over the persistent kernel and the host-driven ablation (race
+detection).  The single-word state discipline is lock-free, so the tools check
+what the design relies on: no out-of-bounds or misaligned access (memcheck), no shared-memory
+hazard inside the CTA-wide phases (racecheck), no divergent or mismatched barrier (synccheck)
+and no read of uninitialised device memory (initcheck).  Runs tests/sanitize_driver.py, which
+also compares every colouring with the oracle."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer(tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    assert os.path.exists(cs), "compute-sanitizer not found"
+    cmd = [cs, "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    r = subprocess.run(cmd + [sys.executable, os.path.join(HERE, "sanitize_driver.py")], capture_output=True,
+                       text=True, timeout=1500)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0, tail
+    assert "sanitize_driver ok" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in (r.stdout + r.stderr), tail
