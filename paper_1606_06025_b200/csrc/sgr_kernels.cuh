@@ -77,6 +77,15 @@ __device__ __forceinline__ void prologue_count(const Params& p, bool dense) {
       }
     }
   }
+  // padding [n, pitch) of the state words, plane 0 and the marks (read, never used, by the
+  // 16-vertex vectors of the dense sweeps); the multi-GPU pre-pass fills whole replicas
+  if (!dist(p)) {
+    for (int64_t v = (int64_t)p.n + (int64_t)blk(p) * BLOCK + threadIdx.x; v < p.plane; v += stride) {
+      sts(st + v, SW<S>::COMMIT);
+      if (PUSH) sts(p.fmp + v, 0u);
+      if (p.dirty) sts(p.dirty + v, 0u);
+    }
+  }
   if (wide) set_status(p, ST_NEED32);
   maxdeg = __reduce_max_sync(FULL, maxdeg);
   if (lane == 0 && maxdeg) {  // multi-GPU: the global max (decides the dirty-set rounds everywhere)
@@ -111,11 +120,16 @@ __device__ __forceinline__ void prologue_dist(const Params& p) {
   }
   if (blk(p) == 0 && threadIdx.x == 0) p.info->gtot[1] = (uint32_t)p.n_global;
 }
+// (the whole pitch: the 16-vertex vectors of the dense sweeps also read the ghost and padding
+// entries of plane 0 and of the marks, whose values they never use)
 template <class S>
 __device__ __forceinline__ void fill_replica(const Params& p) {
   S* st = (S*)p.st;
-  for (int64_t v = (int64_t)blk(p) * BLOCK + threadIdx.x; v < p.n_global; v += (int64_t)nblk(p) * BLOCK)
+  for (int64_t v = (int64_t)blk(p) * BLOCK + threadIdx.x; v < p.plane; v += (int64_t)nblk(p) * BLOCK) {
     sts(st + v, 1u);
+    sts(p.fmp + v, 0u);
+    if (p.dirty) sts(p.dirty + v, 0u);
+  }
 }
 
 // P1: W_1 = V, split into bin segments of wl0 (warp-aggregated cursors; order within a
@@ -227,16 +241,21 @@ __device__ __forceinline__ void store_tent(const Params& p, S* st, int32_t v, ui
   }
 }
 
-// First free colour from the planes, 0 when all np planes are full.
-__device__ __forceinline__ uint32_t plane_firstfit(const Params& p, int32_t v) {
+// First free colour from the planes in Phase A of round r, 0 when all np planes are full.
+// Colours committed before round r are <= r - 1 (a colour c is committed in round >= c, pin
+// P11), so only planes 0..K-1, K = (r - 2) / 8 + 1, can hold any; when they are full the answer
+// is 8K + 1 without reading plane K (which may not even be zeroed yet: plane k is zeroed in
+// Phase A of round 8k, concurrently with this lookup).
+__device__ __forceinline__ uint32_t plane_firstfit(const Params& p, int32_t v, uint32_t r) {
   const uint8_t* f = p.fmp + v;
-  for (uint32_t k = 0; k < p.np; k += 2) {
+  const uint32_t K = min(p.np, r >= 2 ? (r - 2) / 8 + 1 : 1u);
+  for (uint32_t k = 0; k < K; k += 2) {
     const uint32_t b0 = lds(f + (int64_t)k * p.plane);
-    const uint32_t b1 = k + 1 < p.np ? lds(f + (int64_t)(k + 1) * p.plane) : 0xffu;
+    const uint32_t b1 = k + 1 < K ? lds(f + (int64_t)(k + 1) * p.plane) : 0xffu;
     if (b0 != 0xffu) return 8u * k + (uint32_t)__ffs(b0 ^ 0xffu);
     if (b1 != 0xffu) return 8u * (k + 1) + (uint32_t)__ffs(b1 ^ 0xffu);
   }
-  return 0;
+  return K < p.np ? 8u * K + 1u : 0u;
 }
 
 // ---- dirty-set rounds (reading of the data-driven rationale P:453-462)
@@ -315,7 +334,7 @@ __device__ __forceinline__ void phase_a_mask(const Params& p, uint32_t r, const 
         e = ldw(Wb + i);
         t_old = lds(st + e.v) & SW<S>::CMASK;
         if (CW) wk.v[W_WDEG] += (unsigned long long)(RP(p, e.v + 1) - e.beg);
-        const uint32_t t = plane_firstfit(p, e.v);
+        const uint32_t t = plane_firstfit(p, e.v, r);
         if (t) tent_update<S, POL, CW>(p, st, e.v, t, t_old, mark, e.beg, -1, e.k, nchg, wk);
         else fb = true;
       }
@@ -486,7 +505,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           const uint32_t b1 = (pw1[h >> 2] >> ((h & 3) * 8)) & 0xffu;
           const uint32_t t = b0 != 0xffu   ? (uint32_t)__ffs(b0 ^ 0xffu)
                              : b1 != 0xffu ? 8u + (uint32_t)__ffs(b1 ^ 0xffu)
-                                           : plane_firstfit(p, (int32_t)(v0 + h));
+                                           : plane_firstfit(p, (int32_t)(v0 + h), r);
           if (t == 0) {
             fb |= 1u << h;
           } else if (t != (sv & SW<S>::CMASK)) {
@@ -1256,7 +1275,7 @@ __device__ __forceinline__ void phase_a_list(const Params& p, uint32_t r, Work& 
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (sv[u] & SW<S>::COMMIT) continue;
-          const uint32_t t = plane_firstfit(p, v[u]);  // >= 1: 8-bit words, colours <= 8 * np
+          const uint32_t t = plane_firstfit(p, v[u], r);  // >= 1: 8-bit words, colours <= 8 * np
           if (t != (sv[u] & SW<S>::CMASK)) {
             store_tent<S>(p, st, v[u], t);
             chm |= 1u << u;
