@@ -147,9 +147,11 @@ typedef struct gc_opts {
   float* kernel_ms;          /* optional host pointer: device time (CUDA events on the call's
                                 stream) from the first to the last colouring kernel, i.e.
                                 excluding argument checks, copies and validation */
-  uint64_t* phase_ns;        /* optional host pointer [2 * trace_capacity + 1] (diagnostics, with
-                                GC_FLAG_TRACE): device globaltimer (ns) after the ingest and
-                                after Phase A / Phase B of every round, persistent driver only */
+  uint64_t* phase_ns;        /* optional host pointer [4 * trace_capacity + 1] (diagnostics, with
+                                GC_FLAG_TRACE): device globaltimer (ns) after the ingest; per
+                                round r: [4r-3] last CTA done with Phase A's work, [4r-2] its
+                                barrier passed, [4r-1] / [4r] the same for Phase B (persistent
+                                driver only; adds a CTA barrier per phase) */
   const gc_tuning* tuning;   /* optional schedule overrides (NULL = measured defaults) */
   uint64_t reserved[1];
 } gc_opts;

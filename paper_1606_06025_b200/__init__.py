@@ -190,7 +190,7 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
     tr = None
     ph = None
     if phase_times:
-        ph = np.zeros(2 * max(n + 2, 1) + 1, dtype=np.uint64)
+        ph = np.zeros(4 * max(n + 2, 1) + 1, dtype=np.uint64)
         o.phase_ns = ph.ctypes.data
     if trace:
         tr = np.zeros(max(n + 2, 1), dtype=np.uint32)
@@ -215,9 +215,17 @@ def color(row_ptr, col_idx, policy: str = "higher_id", validate: bool = True,
     if time_kernel:
         res.kernel_ms = float(kms.value)
     if phase_times:
-        t = ph[:2 * rd.value + 1].astype(np.int64)
-        res.phase_us = [((t[2 * r + 1] - t[2 * r]) / 1e3 if r > 0 else 0.0, (t[2 * r + 2] - t[2 * r + 1]) / 1e3)
-                        for r in range(rd.value)]
+        # per round: (Phase A us, Phase B us) barrier to barrier, and the part of each spent
+        # after the last CTA finished its work (barrier + tail): (A, B, A_wait, B_wait)
+        t = ph[:4 * rd.value + 1].astype(np.int64)
+        out = []
+        for r in range(1, rd.value + 1):
+            a0 = t[4 * r - 4]  # previous barrier (or ingest end)
+            a = (t[4 * r - 2] - a0) / 1e3 if r > 1 else 0.0
+            aw = (t[4 * r - 2] - t[4 * r - 3]) / 1e3 if r > 1 else 0.0
+            bstart = t[4 * r - 2] if r > 1 else t[0]
+            out.append((a, (t[4 * r] - bstart) / 1e3, aw, (t[4 * r] - t[4 * r - 1]) / 1e3))
+        res.phase_us = out
     return res
 
 

@@ -494,8 +494,8 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.trace_cap = trace ? o.trace_capacity : 0;
   void* dphase = nullptr;
   if (trace && o.phase_ns) {
-    CK(sc.alloc(&dphase, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1)));
-    CK(cudaMemsetAsync(dphase, 0, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1), s));
+    CK(sc.alloc(&dphase, sizeof(uint64_t) * (4 * (size_t)o.trace_capacity + 1)));
+    CK(cudaMemsetAsync(dphase, 0, sizeof(uint64_t) * (4 * (size_t)o.trace_capacity + 1), s));
     p.phase_ns = (unsigned long long*)dphase;
   }
   p.colors_out = (uint32_t*)dcol;
@@ -659,7 +659,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
     }
   }
   if (dphase) {
-    CK(cudaMemcpyAsync(o.phase_ns, dphase, sizeof(uint64_t) * (2 * (size_t)o.trace_capacity + 1),
+    CK(cudaMemcpyAsync(o.phase_ns, dphase, sizeof(uint64_t) * (4 * (size_t)o.trace_capacity + 1),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }

@@ -39,6 +39,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <stddef.h>
 #include <stdint.h>
 
 // The multi-GPU kernel instances (inst_dist_*.cu) are compiled from the same source with
@@ -88,6 +89,9 @@ template <> struct SW<uint32_t> {
 
 // Device-side run state.  Zeroed by the host before launch.
 struct DevInfo {
+  // ---- head (128 B): the values every thread needs after a barrier.  Each CTA copies it to
+  // shared memory once per barrier (grid_sync -> head()), instead of every thread loading the
+  // same L2 line (one L2 slice serialising ~3.5 K warp loads per phase on the stencil).
   uint32_t status;
   uint32_t rounds;
   uint32_t num_colors;
@@ -98,22 +102,25 @@ struct DevInfo {
   uint32_t chg[3];              // tentative colours changed by Phase A, by round (r % 3)
   uint32_t wl_cnt[3];           // list rounds: winners recorded by Phase B, by round (r % 3)
   uint32_t dl_cnt[3];           // list rounds: dirty vertices listed by Phase A, by round (r % 3)
-  uint32_t pad1[7];
-  uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
+  uint32_t gtot[3];             // multi-GPU: global |W| by round (r % 3), summed by the ranks' barrier leaders
+  uint32_t decision;            // status agreed by the last barrier (published with its generation flip)
+  uint32_t pad_h;
   unsigned long long wlp[2];    // the two worklist buffers (re-read every round, see sgr_persistent)
+  // ---- end of head
+  uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
   unsigned long long work[W_N];
   unsigned long long bad;       // validation / verify: ~(smallest offending key), 0 = none
   uint32_t err_code;
-  uint32_t gtot[3];             // multi-GPU: global |W| by round (r % 3), summed by the ranks' barrier leaders
-  uint32_t decision;            // status agreed by the last barrier (published with its generation flip)
   uint32_t diag[4];             // watchdog diagnostics: [0] 1 + rank not heard from, [1] epoch, [2] arrivals seen
-  uint32_t pad2[23];
+  uint32_t pad2[27];
   uint32_t bar_count;           // grid barrier (own 128-B lines)
   uint32_t pad3[31];
   uint32_t bar_gen;
   uint32_t pad4[31];
   uint32_t stage[1024];         // multi-GPU debug: per local CTA, the last step reached (watchdog report)
 };
+
+static_assert(offsetof(DevInfo, qctr) == 128, "DevInfo head must be the first 128 bytes");
 
 // Worklist entry: the vertex, the split k = number of its neighbours with a lower id
 // (-1 = not yet known; rows are sorted so adj(v) = [beg, beg+k) lower ids, [beg+k, end) higher
@@ -170,7 +177,8 @@ struct Params {
   DevInfo* info;
   uint32_t* trace;
   uint32_t trace_cap;
-  unsigned long long* phase_ns;  // diagnostics: [0] = after ingest, [2r-1] after A(r), [2r] after B(r)
+  unsigned long long* phase_ns;  // diagnostics: [0] = after ingest; round r: [4r-3] last CTA done with A(r),
+                                 // [4r-2] A(r) barrier passed, [4r-1] last CTA done with B(r), [4r] B(r) barrier
   uint32_t* colors_out;
   uint32_t max_rounds;
   uint32_t t1;                  // winners of degree <= t1 scatter by themselves, larger: warp-wide
@@ -219,6 +227,13 @@ struct Work {
 };
 
 // ---------------------------------------------------------------- memory helpers
+// This CTA's copy of DevInfo's head as of the last barrier (only the head fields are valid).
+__device__ __forceinline__ uint32_t* head_buf() {
+  __shared__ __align__(16) uint32_t s_head[32];
+  return s_head;
+}
+__device__ __forceinline__ const DevInfo& head() { return *reinterpret_cast<const DevInfo*>(head_buf()); }
+
 
 // Memory access helpers.  Only L1-level hints are used: the L2 cache_hint forms
 // (createpolicy + ld/st/red .L2::cache_hint) were observed to make ptxas 12.9 (sm_100a)
@@ -420,6 +435,19 @@ static __device__ __noinline__ uint32_t xrank_sync(const Params& p, uint32_t gen
   return st;
 }
 
+// Copy DevInfo's head into this CTA's shared head (called by one thread after an acquire).
+__device__ __forceinline__ void take_head(const Params& p) {
+  const uint4* src = reinterpret_cast<const uint4*>(p.info);
+  uint4* dst = reinterpret_cast<uint4*>(head_buf());
+  uint4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w) : "l"(src + i) : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dst[i] = v[i];
+}
+
 static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
   __shared__ uint32_t s_go;
   __syncthreads();
@@ -457,6 +485,7 @@ static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
       if (go) go = ld_relaxed(&I->decision) == ST_OK;
     }
     s_go = go;
+    take_head(p);
   }
   __syncthreads();
   return s_go != 0;

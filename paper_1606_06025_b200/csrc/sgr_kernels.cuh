@@ -426,7 +426,7 @@ __device__ __forceinline__ void phase_a(const Params& p, uint32_t r, const Bins&
   const uint32_t cur = r % 3;
   uint32_t nb[NBIN];
 #pragma unroll
-  for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
+  for (int b = 0; b < NBIN; ++b) nb[b] = head().cnt[cur][b];
   reset_next(p, r);
   if (CW && threadIdx.x == 0 && blk(p) == 0) {
     wk.v[W_A_VERT] += (unsigned long long)nb[0] + nb[1];
@@ -460,7 +460,7 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
   reset_next(p, r);
   if (CW && threadIdx.x == 0 && blk(p) == 0) {
     const uint32_t cur = r % 3;
-    wk.v[W_A_VERT] += (unsigned long long)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+    wk.v[W_A_VERT] += (unsigned long long)head().cnt[cur][0] + head().cnt[cur][1];
     wk.v[W_DA_SWEEP] += (unsigned long long)p.n;
   }
   zero_plane(p, r);
@@ -857,7 +857,7 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   uint32_t nb[NBIN];
 #pragma unroll
-  for (int b = 0; b < NBIN; ++b) nb[b] = ld_relaxed(&p.info->cnt[cur][b]);
+  for (int b = 0; b < NBIN; ++b) nb[b] = head().cnt[cur][b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blk(p) == 0 && threadIdx.x == 0) {
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = nb[0] + nb[1];
@@ -1239,7 +1239,7 @@ __device__ __forceinline__ void phase_a_list(const Params& p, uint32_t r, Work& 
   zero_plane(p, r);
   const int lane = threadIdx.x & 31;
   int32_t* clist = bsmem().clist[threadIdx.x >> 5];
-  const uint32_t nwin = ld_relaxed(&p.info->wl_cnt[(r - 1) % 3]);
+  const uint32_t nwin = head().wl_cnt[(r - 1) % 3];
   const int32_t* WL = ((r - 1) & 1) ? p.wlw1 : p.wlw0;
   uint32_t* q = &p.info->qctr[r % 3][1][0];
   const uint32_t nwarps = nblk(p) * WARPS;
@@ -1307,7 +1307,7 @@ __device__ __forceinline__ void phase_b_list(const Params& p, uint32_t r, uint32
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
     if (CW) wk.v[W_B_VERT] += tot;
   }
-  const uint32_t nd = ld_relaxed(&p.info->dl_cnt[r % 3]);
+  const uint32_t nd = head().dl_cnt[r % 3];
   uint32_t* q = &p.info->qctr[r % 3][0][0];
   const uint32_t nwarps = nblk(p) * WARPS;
   const uint32_t ch = max(1u, min(64u, nd / (4u * nwarps)));
@@ -1350,7 +1350,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
   const uint32_t cur = r % 3, nxt = (r + 1) % 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blk(p) == 0 && threadIdx.x == 0) {
-    const uint32_t tot = ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+    const uint32_t tot = head().cnt[cur][0] + head().cnt[cur][1];
     if (p.trace && r <= p.trace_cap) p.trace[r - 1] = tot;
     if (CW) {
       wk.v[W_B_VERT] += tot;
@@ -1487,7 +1487,7 @@ __device__ __forceinline__ uint32_t next_total(const Params& p, uint32_t r) {
   const uint32_t nxt = (r + 1) % 3;
   uint32_t t = 0;
 #pragma unroll
-  for (int b = 0; b < NBIN; ++b) t += ld_relaxed(&p.info->cnt[nxt][b]);
+  for (int b = 0; b < NBIN; ++b) t += head().cnt[nxt][b];
   return t;
 }
 
@@ -1519,6 +1519,14 @@ __device__ __forceinline__ void flush_work(const Params& p, Work& wk) {
       if ((threadIdx.x & 31) == 0 && x) atomicAdd(&p.info->work[k], x);
     }
   }
+}
+
+// Diagnostics (p.phase_ns): the latest time any CTA of the grid finished the phase's work,
+// before entering the barrier (slot 4r-3: Phase A, 4r-1: Phase B; 4r-2 / 4r: the barrier done).
+__device__ __forceinline__ void work_stamp(const Params& p, uint32_t slot, uint32_t r) {
+  if (!p.phase_ns || r > p.trace_cap) return;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&p.phase_ns[slot], globaltimer());
 }
 
 // ---------------------------------------------------------------- a4: persistent driver
@@ -1562,31 +1570,32 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   bool dense = dense0, list = false;
   uint32_t tot_list = 0;
   // list rounds: 8-bit words (colours from the planes), bounded degree, dirty marks available
-  const bool can_list = sizeof(S) == 1 && PUSH && p.list_ok && p.dirty && ld_relaxed(&p.info->maxdeg) <= 64u;
+  const bool can_list = sizeof(S) == 1 && PUSH && p.list_ok && p.dirty && head().maxdeg <= 64u;
   for (;;) {
-    WE* Win = (WE*)ld_relaxed64(&p.info->wlp[(r + 1) & 1]);
-    WE* Wout = (WE*)ld_relaxed64(&p.info->wlp[r & 1]);
+    WE* Win = (WE*)head().wlp[(r + 1) & 1];
+    WE* Wout = (WE*)head().wlp[r & 1];
     const uint32_t cur = r % 3;
-    const uint64_t tot = list ? tot_list : (uint64_t)ld_relaxed(&p.info->cnt[cur][0]) + ld_relaxed(&p.info->cnt[cur][1]);
+    const uint64_t tot = list ? tot_list : (uint64_t)head().cnt[cur][0] + head().cnt[cur][1];
     // dirty-set rounds (N1) on bounded-degree graphs (max degree <= 64): measured on B200, every
     // round marks on the 27-point stencil (-22 %) and the mesh (-4 %); on R-MAT marking the
     // hub rows costs more than it saves (2.4x slower when forced), and a per-round cost model
     // based on the previous round's tentative-colour changes did no better than this rule
-    bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && ld_relaxed(&p.info->maxdeg) <= 64u));
+    bool mark = r >= 2 && (p.n1 == 2 || (p.n1 == 1 && head().maxdeg <= 64u));
     if (mark && p.n1 == 1 && p.n1chg)  // optional: only once the previous round changed few colours
-      mark = r >= 3 && (uint64_t)ld_relaxed(&p.info->chg[(r - 1) % 3]) * p.n1chg < tot;
+      mark = r >= 3 && (uint64_t)head().chg[(r - 1) % 3] * p.n1chg < tot;
     if (r > 1) {
       if (list) phase_a_list<S, POL, CW>(p, r, wk);
       else if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
       else phase_a<S, POL, PUSH, CW>(p, r, bins, Win, mark, wk);
+      work_stamp(p, 4 * r - 3, r);
       if (!grid_sync(p)) return;
     }
-    if (stamp && r <= p.trace_cap) p.phase_ns[2 * r - 1] = globaltimer();
+    if (stamp && r <= p.trace_cap) p.phase_ns[4 * r - 2] = globaltimer();
     // round r+1 runs as a list round when round r-1's winners x 4 (successors + 1) <= n
     // (p.list_ok == 2: from round 2 on, tests); round r then records its winners
     bool list_next = list;
     if (!list && can_list && r >= 2) {
-      const uint64_t prev = (uint64_t)ld_relaxed(&p.info->cnt[(r - 1) % 3][0]) + ld_relaxed(&p.info->cnt[(r - 1) % 3][1]);
+      const uint64_t prev = (uint64_t)head().cnt[(r - 1) % 3][0] + head().cnt[(r - 1) % 3][1];
       const uint64_t won = prev > tot ? prev - tot : 0;
       list_next = p.list_ok == 2 || won * 4 * p.davg2 <= (uint64_t)p.n;
     }
@@ -1602,12 +1611,13 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
     }
     // multi-GPU: |W_r| of the trace is the global one (the phase wrote the local count)
     if (dist(p) && blk(p) == 0 && threadIdx.x == 0 && p.trace && r <= p.trace_cap)
-      p.trace[r - 1] = ld_relaxed(&p.info->gtot[cur]);
+      p.trace[r - 1] = head().gtot[cur];
+    work_stamp(p, 4 * r - 1, r);
     if (!grid_sync(p, dist(p) ? (int)((r + 1) % 3) : -1)) return;
-    if (stamp && r <= p.trace_cap) p.phase_ns[2 * r] = globaltimer();
+    if (stamp && r <= p.trace_cap) p.phase_ns[4 * r] = globaltimer();
     uint32_t left;
-    if (list) left = (uint32_t)tot - ld_relaxed(&p.info->wl_cnt[cur]);
-    else if (dist(p)) left = ld_relaxed(&p.info->gtot[(r + 1) % 3]);  // global: every rank stops together
+    if (list) left = (uint32_t)tot - head().wl_cnt[cur];
+    else if (dist(p)) left = head().gtot[(r + 1) % 3];  // global: every rank stops together
     else left = next_total(p, r);
     if (list_next) {
       list = true;
@@ -1680,6 +1690,8 @@ __global__ void __launch_bounds__(BLOCK) k_phase_a(Params p, uint32_t r, WE* W) 
   wk.zero();
   Bins b;
   b.load(p);
+  if (threadIdx.x == 0) take_head(p);  // the previous launch's counters
+  __syncthreads();
   phase_a<uint32_t, HIGHER_ID, PUSH, CW>(p, r, b, W, false, wk);
   flush_work<CW>(p, wk);
 }
@@ -1689,6 +1701,8 @@ __global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, WE* W, 
   wk.zero();
   Bins b;
   b.load(p);
+  if (threadIdx.x == 0) take_head(p);  // the previous launch's counters
+  __syncthreads();
   phase_b<uint32_t, POL, PUSH, CW>(p, r, b, W, Wout, false, wk);
   flush_work<CW>(p, wk);
 }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--sweep", default="default")
     ap.add_argument("--barrier", action="store_true")
+    ap.add_argument("--tuning", default="", help="gc_tuning overrides as JSON (phases sweep)")
     args = ap.parse_args()
 
     import torch
@@ -55,13 +56,14 @@ def main():
     variants["densen1"] = [T(dense_div=d, n1=2) for d in (4, 8, 16, 32, 64, 256)]
     variants["misc"] = [dict(), T(scatter_filter=1), T(state_bytes=2), T(variant=0), T(variant=1)]
     if args.sweep == "phases":
-        res = gc.color(rp, ci, validate=False, phase_times=True)
-        tot_a = sum(a for a, b in res.phase_us)
-        tot_b = sum(b for a, b in res.phase_us)
-        print(json.dumps({"config": args.config, "rounds": res.rounds, "phaseA_us": round(tot_a, 1),
-                          "phaseB_us": round(tot_b, 1)}))
-        for r, ((a, b), w) in enumerate(zip(res.phase_us, res.trace), 1):
-            print(f"  r={r:3d} |W|={w:10d} A={a:9.1f}us B={b:9.1f}us")
+        kw = dict(tuning=json.loads(args.tuning)) if args.tuning else {}
+        res = gc.color(rp, ci, validate=False, phase_times=True, **kw)
+        tot = [sum(x[i] for x in res.phase_us) for i in range(4)]
+        print(json.dumps({"config": args.config, "rounds": res.rounds, "phaseA_us": round(tot[0], 1),
+                          "phaseB_us": round(tot[1], 1), "A_after_last_cta_us": round(tot[2], 1),
+                          "B_after_last_cta_us": round(tot[3], 1)}))
+        for r, ((a, b, aw, bw), w) in enumerate(zip(res.phase_us, res.trace), 1):
+            print(f"  r={r:3d} |W|={w:10d} A={a:8.1f}us (barrier {aw:6.1f})  B={b:8.1f}us (barrier {bw:6.1f})")
         return
     for kw in variants[args.sweep]:
         kw = dict(kw)
