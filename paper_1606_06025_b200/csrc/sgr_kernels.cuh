@@ -1539,6 +1539,8 @@ template <class S, int POL, bool PUSH, bool CW>
 __device__ __forceinline__ void sgr_body(const Params& p) {
   Work wk;
   wk.zero();
+  if (threadIdx.x == 0) barriers_passed() = 0;
+  __syncthreads();
   const bool dense0 = PUSH && p.dense_div != 0;
   if (kDist && threadIdx.x == 0) {
     atomicAdd(&p.info->diag[3], 1u);  // CTAs started (watchdog report)
@@ -1713,6 +1715,7 @@ __global__ void __launch_bounds__(BLOCK) k_epilogue(Params p, uint32_t r) {
 
 // Grid-barrier cost probe (diagnostics only: gc__bench_grid_sync).
 __global__ void __launch_bounds__(BLOCK) k_bench_sync(Params p, int iters) {
+  if (threadIdx.x == 0) barriers_passed() = 0;
   for (int i = 0; i < iters; ++i)
     if (!grid_sync(p)) return;
 }
