@@ -41,29 +41,33 @@ def _stale(target, deps):
     return not os.path.exists(target) or any(os.path.getmtime(target) < os.path.getmtime(d) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/*.cu (+ headers) into csrc/libgc.so for sm_100a."""
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile csrc/*.cu (+ headers) into csrc/libgc.so for sm_100a.  `defines` (e.g.
+    ["GC_NQ=1"]) and `out` build a tuning variant elsewhere (A/B measurements only)."""
     units, headers = _units(), _headers()
-    if not force and not _stale(LIB_PATH, units + headers):
-        return LIB_PATH
-    os.makedirs(OBJ, exist_ok=True)
+    lib_path = out or LIB_PATH
+    obj_dir = OBJ if not defines else os.path.join(os.path.dirname(lib_path), "obj_" + "_".join(defines).replace("=", ""))
+    if not force and not defines and not _stale(lib_path, units + headers):
+        return lib_path
+    os.makedirs(obj_dir, exist_ok=True)
     nvcc = _nvcc()
 
     def compile_unit(src):
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         if force or _stale(obj, [src] + headers):
             tmp = obj + f".tmp{os.getpid()}"
-            cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", tmp, src]
+            cmd = [nvcc, *NVCC_FLAGS, *(["-D" + d for d in defines]), *(["-Xptxas=-v"] if verbose else []), "-c", "-o",
+                   tmp, src]
             subprocess.check_call(cmd)
             os.replace(tmp, obj)
         return obj
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(units), os.cpu_count() or 1))) as ex:
         objs = list(ex.map(compile_unit, units))
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    tmp = lib_path + f".tmp{os.getpid()}"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 def load() -> ctypes.CDLL:

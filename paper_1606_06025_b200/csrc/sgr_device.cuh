@@ -70,6 +70,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int32_t NARROW_MAX_DEG = 32766;  // 16-bit state: colours <= Delta+1 <= 32767
 
 enum Policy { HIGHER_ID = 0, LOWER_ID = 1, DEGREE = 2 };
+
 constexpr int MAX_PLANES = 64;     // byte planes of forbidden colours: colours 1..512
 enum Status { ST_OK = 0, ST_NEED16 = 2, ST_NO_CONVERGENCE = 3, ST_NEED32 = 4, ST_WATCHDOG = 5 };
 enum WorkIdx { W_A_VERT = 0, W_A_EDGE, W_B_VERT, W_B_EDGE, W_B_GATHER, W_SCATTER, W_PUSH, W_SCATTER_RED,
@@ -107,7 +108,7 @@ struct DevInfo {
   uint32_t pad_h;
   unsigned long long wlp[2];    // the two worklist buffers (re-read every round, see sgr_persistent)
   // ---- end of head
-  uint32_t qctr[3][NBIN][32];   // Phase-B work-queue heads per bin (own 128-B lines), by r % 3
+  uint32_t qctr[3][NBIN][32];   // work-queue heads (own 128-B lines), by r % 3 ([1]: list rounds)
   unsigned long long work[W_N];
   unsigned long long bad;       // validation / verify: ~(smallest offending key), 0 = none
   uint32_t err_code;

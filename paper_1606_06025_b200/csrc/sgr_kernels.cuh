@@ -304,6 +304,10 @@ __device__ __forceinline__ void tent_update(const Params& p, S* st, int32_t v, u
 }
 
 __device__ __forceinline__ void flush_chg(const Params& p, uint32_t r, uint32_t nchg, Work& wk, bool cw) {
+#ifndef GC_FLUSH_CHG
+#define GC_FLUSH_CHG 0
+#endif
+  if (!GC_FLUSH_CHG && !cw && !p.n1chg) return;  // only the N1_CHG rule and the work counters read it
   nchg = __reduce_add_sync(FULL, nchg);
   if ((threadIdx.x & 31) == 0 && nchg) {
     atomicAdd(&p.info->chg[r % 3], nchg);
@@ -623,6 +627,24 @@ __device__ __forceinline__ uint32_t pop_chunk(uint32_t* q, uint32_t ch, int lane
   uint32_t b = 0;
   if (lane == 0) b = atomicAdd(q, ch);
   return __shfl_sync(FULL, b, 0);
+}
+
+// Adds the per-warp values (lane 0's v) of the whole CTA to *g with one atomic per CTA.  Every
+// thread of the CTA must call it.
+#ifndef GC_CTA_ADD
+#define GC_CTA_ADD 1
+#endif
+__device__ __forceinline__ void cta_add(uint32_t* g, uint32_t v) {
+  if (!GC_CTA_ADD) {
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(g, v);
+    return;
+  }
+  __shared__ uint32_t s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_sum, v);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_sum) atomicAdd(g, s_sum);
 }
 
 // Position of the j-th entry of a scan range in scan order.
@@ -1404,7 +1426,17 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
     int32_t* clist = sm.clist[warp];
     int* s_first = sm.cwfirst[warp];
     constexpr uint32_t CHD = 512;
-    for (uint32_t c0 = pop_chunk(q, CHD, lane); c0 < nv; c0 = pop_chunk(q, CHD, lane)) {
+    // chunks dealt out statically, interleaved over the warps: a dynamic queue head costs one
+    // same-address atomic per chunk and warp (mesh 8192^2: ~130 K per round, serialised at one
+    // L2 slice), and the interleaving spreads the dirty band of the colouring front evenly
+    // (with few chunks per warp the dynamic queue balances better: up to GC_DIRTY_DYN chunks per warp)
+#ifndef GC_DIRTY_DYN
+#define GC_DIRTY_DYN 4
+#endif
+    const uint32_t gw = blk(p) * WARPS + warp, nch = (nv + CHD - 1) / CHD;
+    const bool dyn = nch <= GC_DIRTY_DYN * nwarps;
+    for (uint32_t ck = dyn ? pop_chunk(q, 1, lane) : gw; ck < nch; ck = dyn ? pop_chunk(q, 1, lane) : ck + nwarps) {
+      const uint32_t c0 = ck * CHD;
       const uint32_t v0 = lo16 + c0 + 16u * lane;
       uint32_t cand = 0, pend = 0;
       if (v0 < vend) {
@@ -1468,7 +1500,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
       const uint32_t np = __reduce_add_sync(FULL, (uint32_t)__popc(pend) - heavy_pend);
       lost_cnt += np - won;
     }
-    if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
+    cta_add(&cnt_next[0], lane == 0 ? lost_cnt : 0u);
     return;
   }
   const uint32_t ch = max((uint32_t)WB, min(2048u, (nv / (p.dch * nwarps)) / WB * WB));
@@ -1479,7 +1511,7 @@ __device__ __forceinline__ void phase_b_dense(const Params& p, uint32_t r, const
                                      r == 1);
   }
   if (push_out) pu.template flush<CW>(lane, wk.v[W_PUSH]);
-  else if (lane == 0 && lost_cnt) atomicAdd(&cnt_next[0], lost_cnt);
+  else cta_add(&cnt_next[0], lane == 0 ? lost_cnt : 0u);
 }
 
 // |W_{r+1}| summed over bins (read after the barrier that ends Phase B of round r).
