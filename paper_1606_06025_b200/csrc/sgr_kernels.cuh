@@ -893,11 +893,11 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
   pu.init(sm.pbuf[warp], Wout, cnt_next, bins);
 
   // bin 1 first (one CTA per vertex, high degrees: the longest items start early), then the
-  // dynamic bin-0 queue fills the gaps
-  {
-    const WE* Wb = W + bins.off[1];
-    WE* Ob = Wout + bins.off[1];
-    for (uint32_t i = blk(p); i < nb[1]; i += nblk(p)) {
+  // dynamic bin-0 queue fills the gaps.  Tail rounds (no more pending vertices than CTAs: the
+  // last, high-degree vertices with long scans and scatters) give every vertex a CTA.
+  const bool tail = nb[0] + nb[1] <= nblk(p);
+  auto cta_loop = [&](const WE* Wb, uint32_t cnt, uint32_t* outc, WE* Ob, uint32_t first) {
+    for (uint32_t i = (blk(p) + first) % nblk(p); i < cnt; i += nblk(p)) {
       WE e = ldw(Wb + i);
       if (threadIdx.x == 0) {  // one read of the state word and the dirty mark, broadcast
         uint32_t x = lds(st + e.v) & SW<S>::CMASK;
@@ -913,11 +913,17 @@ __device__ __forceinline__ void phase_b(const Params& p, uint32_t r, const Bins&
       if (CW && threadIdx.x == 0 && !(tx & 0x40000000u)) wk.v[W_B_EVAL] += 1;
       if (((tx & 0x40000000u) || cta_vertex<S, POL, PUSH, CW>(p, e, tx, wk, &sm.first, &sm.k, rec_round)) &&
           threadIdx.x == 0) {
-        stw(Ob + atomicAdd(&cnt_next[1], 1u), e);
+        stw(Ob + atomicAdd(outc, 1u), e);
         if (CW) wk.v[W_PUSH] += 1;
       }
       __syncthreads();
     }
+  };
+  cta_loop(W + bins.off[1], nb[1], &cnt_next[1], Wout + bins.off[1], 0);
+  if (tail) {
+    // a split still unknown (-1, first visit) is found by cta_vertex
+    cta_loop(W + bins.off[0], nb[0], &cnt_next[0], Wout + bins.off[0], nb[1]);
+    return;
   }
   phase_b_coop<S, POL, PUSH, CW>(p, W + bins.off[0], nb[0], &p.info->qctr[cur][0][0], pu, mark, wk, sm.cwfirst[warp],
                                  rec_round);
