@@ -3,7 +3,10 @@ detection).  The single-word state discipline is lock-free, so
 what the design relies on: no out-of-bounds or misaligned access (memcheck), no shared-memory
 hazard inside the CTA-wide phases (racecheck), no divergent or mismatched barrier (synccheck)
 and no read of uninitialised device memory (initcheck).  Runs tests/sanitize_driver.py, which
-also compares every colouring with the oracle."""
+also compares every colouring with the oracle.
+
+Opt-in (GC_RUN_SANITIZER=1): the GPU pool wraps compute-sanitizer and may close it (runs under
+it have left pool GPUs needing a reset); the wrapper then exits 86 and the test is skipped."""
 import os
 import shutil
 import subprocess
@@ -17,6 +20,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer(tool):
+    if os.environ.get("GC_RUN_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer runs are opt-in (GC_RUN_SANITIZER=1)")
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     assert os.path.exists(cs), "compute-sanitizer not found"
     cmd = [cs, "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
@@ -25,6 +30,8 @@ def test_compute_sanitizer(tool):
     r = subprocess.run(cmd + [sys.executable, os.path.join(HERE, "sanitize_driver.py")], capture_output=True,
                        text=True, timeout=1500)
     tail = (r.stdout + r.stderr)[-4000:]
+    if r.returncode == 86 and "closed on this pool" in tail:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert r.returncode == 0, tail
     assert "sanitize_driver ok" in r.stdout, tail
     out = r.stdout + r.stderr
