@@ -144,7 +144,9 @@ def algorithmic_bytes(work, n):
                sparse, per entry         : WE 16 + sw
                per examined position     : col 4 + sw
                per vertex (commit, once) : sw;  per pushed loser : WE 16
-               per scatter edge          : col 4 + RED 4
+               per scatter edge issued   : col 4 + RED 4 (scatter_reds: edges into neighbours
+                                           seen committed by the winner's own scan are skipped,
+                                           neither loaded nor REDed — GC_RFILT)
       finalize per vertex : sw + colour 4
     """
     sw = int(work.get("state_bytes") or 1)
@@ -154,7 +156,7 @@ def algorithmic_bytes(work, n):
             + sw * work["phase_a_vertices"] + (4 + sw) * work["phase_a_edges"]
             + sw * work["dense_b_swept"] + 12 * dense_b_pending + (16 + sw) * work["sparse_b_entries"]
             + (4 + sw) * work["phase_b_edges"] + sw * n + 16 * work["pushes"]
-            + 8 * work["commit_scatter"]
+            + 8 * work.get("scatter_reds", work["commit_scatter"])
             + (sw + 4) * n)
 
 

@@ -86,7 +86,10 @@ typedef struct gc_work {
   uint64_t phase_b_gathers;    /* neighbour colour words gathered by the conflict scans */
   uint64_t commit_scatter;     /* neighbour entries visited by the commit scatters */
   uint64_t pushes;             /* vertices pushed into W_out over the run */
-  uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters */
+  uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters (entries whose neighbour
+                                   the winner saw committed during its own scan are skipped; a
+                                   neighbour committing in the same phase may be seen either way,
+                                   so this one counter can vary between runs) */
   uint64_t dense_a_swept;      /* vertices swept by dense (id-order) Phase A passes */
   uint64_t dense_b_swept;      /* vertices swept by dense Phase B passes */
   uint64_t sparse_a_entries;   /* worklist entries read by sparse Phase A passes */
@@ -121,7 +124,9 @@ typedef struct gc_tuning {
   int32_t variant;         /* kernel: 0 = 4 CTAs/SM, 1 = 3 CTAs/SM (80 registers); -1 = chosen by a
                               max-degree pre-pass (bounded degree <= 64 and m >= 8n -> 1) */
   int32_t watchdog_ms;     /* device watchdog per grid barrier, ms (0 or -1: 60 000); tests use less */
-  int32_t reserved[4];
+  int32_t widen;           /* 8-bit words overflowing (a colour > 127): 1 (default) widen them to 16 bits
+                              in place and resume at the Phase A that overflowed; 0 restart the run */
+  int32_t reserved[3];
 } gc_tuning;
 
 /* Fill *t with "defaults" (-1 / 0 as above). */

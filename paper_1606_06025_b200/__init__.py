@@ -60,7 +60,7 @@ class Tuning(ctypes.Structure):
                 ("dense_div", ctypes.c_int32), ("dense_div_n1", ctypes.c_int32), ("n1", ctypes.c_int32),
                 ("list", ctypes.c_int32), ("compact", ctypes.c_int32), ("scatter_filter", ctypes.c_int32),
                 ("dch", ctypes.c_int32), ("n1_chg", ctypes.c_int32), ("variant", ctypes.c_int32),
-                ("watchdog_ms", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("watchdog_ms", ctypes.c_int32), ("widen", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class Opts(ctypes.Structure):

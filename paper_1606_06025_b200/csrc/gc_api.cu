@@ -204,6 +204,7 @@ struct Knobs {
   uint32_t dense_div = 3, dense_div_n1 = 16, n1 = 1, list = 0, compact = 0, sfilter = 0, dch = 16, n1_chg = 0;
   int variant = -1;
   uint32_t watchdog_ms = 0;  // 0 = 60 s
+  uint32_t widen = 1;        // 8-bit overflow: widen in place and resume (1) or restart (0)
 };
 bool resolve_knobs(const gc_tuning* t, Knobs* k) {
   *k = Knobs();
@@ -221,6 +222,7 @@ bool resolve_knobs(const gc_tuning* t, Knobs* k) {
   if (t->n1_chg >= 0) k->n1_chg = (uint32_t)t->n1_chg;
   k->variant = t->variant < 0 ? -1 : (t->variant ? 1 : 0);
   if (t->watchdog_ms > 0) k->watchdog_ms = (uint32_t)t->watchdog_ms;
+  if (t->widen >= 0) k->widen = t->widen ? 1u : 0u;
   return true;
 }
 
@@ -261,6 +263,7 @@ void gc_tuning_default(gc_tuning* t) {
   t->state_bytes = 0;
   t->dense_div = t->dense_div_n1 = t->n1 = t->list = t->compact = t->scatter_filter = t->dch = t->n1_chg = -1;
   t->variant = -1;
+  t->widen = -1;
 }
 
 void gc_opts_default(gc_opts* o) {
@@ -553,6 +556,9 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       p.st = (uint8_t*)planes - (int64_t)sbytes * pitch;
       void* fn = pick_persistent(sbytes, (int)o.policy, push, cw, fat);
       int per_sm = 0;
+#ifdef GC_CARVEOUT
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, GC_CARVEOUT));
+#endif
       CK(occupancy(dev, fn, &per_sm));
       if (per_sm < 1) {
         set_err("gc_color: persistent kernel cannot be resident");
@@ -562,13 +568,42 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       const int grid = prop.sms * per_sm;
       void* args[] = {&p};
       CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s));
-      uint32_t status = 0;
-      CK(cudaMemcpyAsync(&status, &((DevInfo*)info)->status, sizeof(status), cudaMemcpyDeviceToHost, s));
+      uint32_t status = 0, rsm[2] = {0, 0};
+      DevInfo* I = (DevInfo*)info;
+      CK(cudaMemcpyAsync(&status, &I->status, sizeof(status), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(rsm, &I->resume_r, sizeof(rsm), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       sbytes_used = sbytes;
-      if (status == ST_NEED16 && sbytes < 2) sbytes = 2;
-      else if (status == ST_NEED32 && sbytes < 4) sbytes = 4;
-      else break;
+      if (status == ST_NEED16 && sbytes < 2) {
+        sbytes = 2;
+        // The 8-bit run stopped at the barrier after Phase A of round rsm[0] (a colour > 127):
+        // widen its state words in place and let the 16-bit kernel resume at that Phase A, instead
+        // of repeating rounds 1..rsm[0]-1 (the words sit right before plane 0 in both widths, so
+        // the 8-bit copy goes through a temporary).  Not with exact work counters (they would
+        // count that Phase A twice): those runs restart.
+        if (kn.widen && !cw && rsm[0] >= 2) {
+          void* tmp;
+          CK(sc.alloc(&tmp, (size_t)pitch));
+          CK(cudaMemcpyAsync(tmp, planes - pitch, (size_t)pitch, cudaMemcpyDeviceToDevice, s));
+          k_widen8<<<prop.sms * 8, BLOCK, 0, s>>>((const uint8_t*)tmp, (uint16_t*)(planes - 2 * pitch), pitch);
+          CK(cudaGetLastError());
+          // the run goes on: clear the stop status and the barrier counter (the 16-bit grid may
+          // differ in size); the aborted Phase A's change count is redone
+          CK(cudaMemsetAsync(&I->status, 0, sizeof(I->status), s));
+          CK(cudaMemsetAsync(I->pstatus, 0, sizeof(I->pstatus), s));
+          CK(cudaMemsetAsync(&I->bar_count, 0, sizeof(I->bar_count), s));
+          CK(cudaMemsetAsync(&I->chg[rsm[0] % 3], 0, sizeof(uint32_t), s));
+          CK(cudaMemsetAsync(&I->resume_r, 0, 2 * sizeof(uint32_t), s));
+          p.resume_r = rsm[0];
+          p.resume_dense = rsm[1];
+          continue;
+        }
+      } else if (status == ST_NEED32 && sbytes < 4) {
+        sbytes = 4;
+      } else {
+        break;
+      }
+      p.resume_r = 0;
       CK(cudaMemsetAsync(info, 0, sizeof(DevInfo), s));
     }
   } else {

@@ -114,7 +114,9 @@ struct DevInfo {
   uint32_t err_code;
   uint32_t diag[4];             // watchdog diagnostics: [0] 1 + rank not heard from, [1] epoch, [2] arrivals seen
   uint32_t pstatus[2];          // one GPU: status raised before barrier k, in slot k & 1 (read after barrier k)
-  uint32_t pad2[25];
+  uint32_t resume_r;            // 8-bit run stopped by ST_NEED16 after Phase A of this round (0: not resumable)
+  uint32_t resume_mode;         //   ... in a dense (1) or sparse (0) round
+  uint32_t pad2[23];
   uint32_t bar_count;           // grid barrier (own 128-B lines)
   uint32_t pad3[31];
   uint32_t bar_gen;
@@ -183,6 +185,8 @@ struct Params {
                                  // [4r-2] A(r) barrier passed, [4r-1] last CTA done with B(r), [4r] B(r) barrier
   uint32_t* colors_out;
   uint32_t max_rounds;
+  uint32_t resume_r;            // != 0: continue a run widened from 8-bit words at Phase A of this round
+  uint32_t resume_dense;        //   ... dense (1) or sparse (0)
   uint32_t t1;                  // winners of degree <= t1 scatter by themselves, larger: warp-wide
   uint32_t t3;                  // degree <= t3: bin 0 (thread + warp); above: bin 1 (one CTA)
   unsigned long long timeout_ns;
@@ -318,6 +322,34 @@ __device__ __forceinline__ void sts(uint16_t* p, uint32_t v) {
 __device__ __forceinline__ void sts(uint32_t* p, uint32_t v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Phase-B conflict-scan gathers of neighbour state words.  Only the colour bits are used, and
+// they are fixed from the barrier that ends Phase A to the one that ends Phase B (Phase B only
+// sets commit bits), so these loads may be served by L1 (GC_L1_GATHER): every grid barrier
+// acquires at gpu scope, which invalidates the SM's L1 (CCTL.IVALL), so no line read before the
+// barrier survives into the phase.  Narrow (8/16-bit) words only: the 32-bit words are also used
+// by the host-driven ablation, whose launches have no such barrier.
+#ifndef GC_L1_GATHER
+#define GC_L1_GATHER 0
+#endif
+__device__ __forceinline__ uint32_t ldnb(const uint8_t* p) {
+#if GC_L1_GATHER
+  uint32_t v;
+  asm volatile("ld.global.ca.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+#else
+  return lds(p);
+#endif
+}
+__device__ __forceinline__ uint32_t ldnb(const uint16_t* p) {
+#if GC_L1_GATHER
+  uint16_t v;
+  asm volatile("ld.global.ca.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v;
+#else
+  return lds(p);
+#endif
+}
+__device__ __forceinline__ uint32_t ldnb(const uint32_t* p) { return lds(p); }
 __device__ __forceinline__ int32_t ldks(const int32_t* p) {
   int32_t v;
   asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -482,7 +514,12 @@ static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
       const uint32_t target = (old / G + 1) * G;
       uint32_t go = 1;
       const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire(&I->bar_count) - target) < 0) {
+#ifndef GC_BAR_RELAXED_SPIN
+#define GC_BAR_RELAXED_SPIN 1
+#endif
+      // spin with relaxed loads and acquire once at the end: every acquire invalidates the SM's
+      // L1 (CCTL.IVALL), which would also evict the lines of the CTAs still working on this SM
+      while ((int32_t)((GC_BAR_RELAXED_SPIN ? ld_relaxed(&I->bar_count) : ld_acquire(&I->bar_count)) - target) < 0) {
         if (globaltimer() - t0 > p.timeout_ns) {
           I->diag[2] = ld_relaxed(&I->bar_count);
           atomicExch(&I->status, (uint32_t)ST_WATCHDOG);
@@ -490,6 +527,7 @@ static __device__ __noinline__ bool grid_sync(const Params& p, int nxt = -1) {
           break;
         }
       }
+      if (GC_BAR_RELAXED_SPIN) (void)ld_acquire(&I->bar_count);  // synchronizes with every arrival (release sequence)
       const uint32_t bk = barriers_passed() + 1;
       barriers_passed() = bk;
       if (go) go = ld_relaxed(&I->pstatus[bk & 1]) == ST_OK;
@@ -776,7 +814,7 @@ __device__ __forceinline__ bool conflict_cta(const Params& p, int32_t v, uint32_
     bool hit = false;
     if (valid) {
       const int32_t w = ldc(p.ci, down ? hi - 1 - j : lo + j);
-      hit = (lds(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
+      hit = (ldnb(st + w) & SW<S>::CMASK) == tent && recolors<POL>(p, v, w, dv);
     }
     if (CW) {
       if (threadIdx.x == 0) *s_first = BLOCK;

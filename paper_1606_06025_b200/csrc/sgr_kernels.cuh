@@ -197,6 +197,15 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
 #ifndef GC_VPL
 #define GC_VPL 2
 #endif
+#ifndef GC_RFILT
+#define GC_RFILT 0
+#endif
+#ifndef GC_CMSMEM
+#define GC_CMSMEM 1
+#endif
+#ifndef GC_SYNC_SCATTER
+#define GC_SYNC_SCATTER 1
+#endif
 constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
 constexpr int WB = 32 * VPL;    // vertices per warp batch
 struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
@@ -208,6 +217,9 @@ struct WideSeg {                // per-warp segment table of one dense batch (sl
   int first[WB];                // work counters: first hit
   uint32_t tent[WB];
   uint32_t lost[VPL];
+#if GC_CMSMEM
+  uint32_t cm[WB][2];           // scan positions 0..63 whose neighbour was seen committed (GC_RFILT)
+#endif
 };
 struct BSmem {
   WE pbuf[WARPS][PBUF];   // per-warp push staging (Pusher, bin 0)
@@ -218,6 +230,9 @@ struct BSmem {
   int first;              // conflict_cta
   int32_t k;              // cta_vertex split broadcast
   int cwfirst[WARPS][32]; // work counters: first hit per lane's vertex
+#if GC_CMSMEM
+  uint32_t cm[WARPS][64];  // sparse batches: per lane, scan positions 0..63 seen committed (GC_RFILT)
+#endif
 };
 __device__ __forceinline__ BSmem& bsmem() {
   __shared__ BSmem s;
@@ -513,10 +528,13 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           if (t == 0) {
             fb |= 1u << h;
           } else if (t != (sv & SW<S>::CMASK)) {
-            if (sizeof(S) == 1 && t > SW<S>::CMASK) set_status(p, ST_NEED16);
-            w[wi] = (w[wi] & ~(SMASK << sh)) | ((t & SMASK) << sh);
-            dirty = true;
-            chgm |= 1u << h;
+            if (sizeof(S) == 1 && t > SW<S>::CMASK) {
+              set_status(p, ST_NEED16);  // the word keeps its old value: the run is widened and resumed here
+            } else {
+              w[wi] = (w[wi] & ~(SMASK << sh)) | ((t & SMASK) << sh);
+              dirty = true;
+              chgm |= 1u << h;
+            }
           }
         }
       }
@@ -663,6 +681,19 @@ __device__ __forceinline__ void rec_winners(const Params& p, uint32_t r, bool wi
   if (win) ((r & 1) ? p.wlw1 : p.wlw0)[pos + __popc(m & lanemask_lt())] = v;
 }
 
+// Commit-scatter filter (GC_RFILT): a winner has examined its whole scan range, so it knows which
+// of those neighbours were committed (before or during this phase).  A committed vertex never
+// reads its forbidden-colour planes again, so the RED into its plane byte is useless (about a
+// third of all REDs on R-MAT): the scans record "committed" for scan positions 0..63 in a
+// per-slot 64-bit mask in shared memory and the scatter skips those neighbours.  Row offset x of
+// the owner's row maps to scan position j (HIGHER_ID: k-1-x below the split; LOWER_ID: x-k above
+// it; DEGREE: x); positions outside [0, 64) are always scattered.
+template <int POL>
+__device__ __forceinline__ bool rfilt_skip(const uint32_t* cm2, int64_t x, int32_t k) {
+  const int64_t j = POL == HIGHER_ID ? (int64_t)k - 1 - x : (POL == LOWER_ID ? x - k : x);
+  return j >= 0 && j < 64 && ((cm2[j >> 5] >> (j & 31)) & 1u);
+}
+
 // One batch of up to 32 vertices, one per lane (act).  The conflict scans of all of them
 // advance together in passes over the flattened segments: pass 1 examines the first 4
 // positions of every scan range (the nearest lower ids, where most conflicts are), later
@@ -689,6 +720,13 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     if (POL == DEGREE) dv = end - e.beg;
     state = len ? 3 : 2;
   }
+#if GC_RFILT
+  uint32_t* const cmw = bsmem().cm[threadIdx.x >> 5];
+#else
+  uint32_t* const cmw = nullptr;
+#endif
+  constexpr bool RF = GC_RFILT && PUSH;
+  if (RF) { cmw[2 * lane] = 0; cmw[2 * lane + 1] = 0; }
   // conflict-scan passes
   uint32_t cap = PROBE;
   for (;;) {
@@ -723,7 +761,9 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         const uint32_t to = __shfl_sync(FULL, tent, oc);
         const int32_t vo = __shfl_sync(FULL, e.v, oc);
         const int64_t dvo = POL == DEGREE ? __shfl_sync(FULL, dv, oc) : 0;
-        const bool hit = own[u] >= 0 && (lds(st + w[u]) & CM) == to && recolors<POL>(p, vo, w[u], dvo);
+        const uint32_t sv = own[u] >= 0 ? ldnb(st + w[u]) : 0u;
+        const bool hit = own[u] >= 0 && (sv & CM) == to && recolors<POL>(p, vo, w[u], dvo);
+        if (RF && (sv & SW<S>::COMMIT) && jj[u] < 64) atomicOr(&cmw[2 * oc + (int)(jj[u] >> 5)], 1u << (jj[u] & 31));
         if (hit) {
           lost |= 1u << oc;
           if (CW) atomicMin(&s_first[oc], (int)jj[u]);
@@ -757,9 +797,10 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     const bool sc = win && tent <= 8u * p.np;
     if (sc && end < 0) end = RP(p, e.v + 1);
     const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
-    if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wn; }
+    if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter && !RF) wk.v[W_SCATTER_RED] += Wn; }
     const uint32_t E = warp_incl_scan(Wn, lane);
     const uint32_t T = __shfl_sync(FULL, E, 31);
+    if (GC_SYNC_SCATTER || RF) __syncwarp();  // the scans' committed masks (RF)
     for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
       int32_t w[4];
       uint32_t wb[4];
@@ -772,8 +813,10 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
         const int64_t bo = __shfl_sync(FULL, e.beg, oc);
         const uint32_t to = __shfl_sync(FULL, tent, oc);
+        const int32_t ko = RF ? __shfl_sync(FULL, e.k, oc) : 0;
         wb[u] = 1u << ((to - 1) & 7);
-        w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
+        const bool skip = RF && f < T && rfilt_skip<POL>(cmw + 2 * oc, (int64_t)(f - (Eo - Wo)), ko);
+        w[u] = f < T && !skip ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
         pl[u] = (dist(p) && w[u] >= 0 ? fmp_of(p, w[u]) : p.fmp) + (int64_t)((to - 1) >> 3) * p.plane;
       }
       if (p.sfilter) {
@@ -789,7 +832,10 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (w[u] >= 0) red_plane<S>(pl[u], w[u], wb[u]);
+          if (w[u] >= 0) {
+            red_plane<S>(pl[u], w[u], wb[u]);
+            if (CW && RF) wk.v[W_SCATTER_RED] += 1;
+          }
       }
     }
   }
@@ -1045,11 +1091,17 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       if (((states >> (8 * h)) & 0xffu) != 3u) continue;
       const uint32_t t = sg.tent[sl];
       int first = -1;
+      uint32_t cbits = 0;
 #pragma unroll
-      for (int u = PROBE - 1; u >= 0; --u)
-        if (w[h][u] >= 0 && (lds(st + w[h][u]) & CM) == t &&
-            recolors<POL>(p, (int32_t)(base + sl), w[h][u], (int64_t)sg.deg[sl]))
+      for (int u = PROBE - 1; u >= 0; --u) {
+        const uint32_t sv = w[h][u] >= 0 ? ldnb(st + w[h][u]) : 0u;
+        if (GC_RFILT && PUSH && (sv & SW<S>::COMMIT)) cbits |= 1u << u;
+        if (w[h][u] >= 0 && (sv & CM) == t && recolors<POL>(p, (int32_t)(base + sl), w[h][u], (int64_t)sg.deg[sl]))
           first = u;
+      }
+#if GC_RFILT
+      if (PUSH) { sg.cm[sl][0] = cbits; sg.cm[sl][1] = 0; }
+#endif
       const uint32_t len = seg_len<POL>(sg, sl);
       if (first >= 0) {
         states ^= 2u << (8 * h);  // 3 -> 1
@@ -1100,8 +1152,11 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       for (int u = 0; u < FLAT_U; ++u) {
         if (own[u] >= 0) {
           const int o = own[u];
-          const bool hit = (lds(st + w[u]) & CM) == sg.tent[o] &&
-                           recolors<POL>(p, (int32_t)(base + o), w[u], (int64_t)sg.deg[o]);
+          const uint32_t sv = ldnb(st + w[u]);
+          const bool hit = (sv & CM) == sg.tent[o] && recolors<POL>(p, (int32_t)(base + o), w[u], (int64_t)sg.deg[o]);
+#if GC_RFILT
+          if (PUSH && (sv & SW<S>::COMMIT) && jj[u] < 64) atomicOr(&sg.cm[o][jj[u] >> 5], 1u << (jj[u] & 31));
+#endif
           if (hit) {
             atomicOr(&sg.lost[o >> 5], 1u << (o & 31));
             if (CW) atomicMin(&sg.first[o], (int)jj[u]);
@@ -1147,7 +1202,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     for (int h = 0; h < VPL; ++h) {
       const int sl = lane * VPL + h;
       Wh[h] = ((states >> (8 * h)) & 0xffu) == 2u && sg.tent[sl] <= 8u * p.np ? sg.deg[sl] : 0u;
-      if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wh[h]; }
+      if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter && !GC_RFILT) wk.v[W_SCATTER_RED] += Wh[h]; }
     }
     const uint32_t T = seg_prefix(sg, Wh, lane);
     for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
@@ -1161,7 +1216,11 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
         if (f < T) {
           const int o = seg_owner(sg.E, f);
           own[u] = o;
-          w[u] = ldc(p.ci, seg_beg<POL>(sg, o) + (f - (o ? sg.E[o - 1] : 0u)));
+          const uint32_t x = f - (o ? sg.E[o - 1] : 0u);
+#if GC_RFILT
+          if (rfilt_skip<POL>(sg.cm[o], (int64_t)x, sg.k[o])) continue;
+#endif
+          w[u] = ldc(p.ci, seg_beg<POL>(sg, o) + x);
         }
       }
       uint32_t skip = 0;
@@ -1175,7 +1234,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
         if (w[u] < 0 || (skip >> u & 1u)) continue;
         const uint32_t t = sg.tent[own[u]];
         red_color<S>(p, (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
-        if (CW && p.sfilter) wk.v[W_SCATTER_RED] += 1;
+        if (CW && (p.sfilter || GC_RFILT)) wk.v[W_SCATTER_RED] += 1;
       }
     }
     __syncwarp();
@@ -1580,6 +1639,20 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   if (threadIdx.x == 0) barriers_passed() = 0;
   __syncthreads();
   const bool dense0 = PUSH && p.dense_div != 0;
+  uint32_t r = 1;
+  bool dense = dense0;
+  Bins bins;
+  if (p.resume_r) {
+    // continuation of an 8-bit run stopped by ST_NEED16 after Phase A of round resume_r: the host
+    // widened the state words in place; every other array (planes, marks, worklists, counters in
+    // DevInfo) is as that run left it.  Phase A of the round is redone with the wider words.
+    if (threadIdx.x == 0) take_head(p);
+    __syncthreads();
+    bins.load(p);
+    r = p.resume_r;
+    dense = p.resume_dense != 0;
+    goto rounds;
+  }
   if (kDist && threadIdx.x == 0) {
     atomicAdd(&p.info->diag[3], 1u);  // CTAs started (watchdog report)
     p.info->stage[blk(p) & 1023] = 1;
@@ -1593,21 +1666,20 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
   }
   prologue_count<S, POL, PUSH>(p, dense0);
   if (!grid_sync(p)) return;
-  Bins bins;
   bins.load(p);
   if (!dense0) prologue_scatter(p, bins);
   else if (blk(p) == 0 && threadIdx.x < NBIN) p.info->cnt[1][threadIdx.x] = bins.size[threadIdx.x];
   if (!grid_sync(p)) return;
+rounds:
   const bool stamp = p.phase_ns && blk(p) == 0 && threadIdx.x == 0;
-  if (stamp) p.phase_ns[0] = globaltimer();
+  if (stamp && !p.resume_r) p.phase_ns[0] = globaltimer();
 
   // The worklist pointers are re-read from DevInfo every round instead of being swapped in
   // registers: with loop-carried pointer swaps, ptxas (12.9) was observed to reuse the
   // uniform register holding one of them inside the grid barrier (truncated addresses).
   // Rounds run dense (W_r implicit, id-order sweeps) while |W_r| * dense_div > n, then
   // sparse (worklists); the round whose |W_r| first falls below pushes its losers.
-  uint32_t r = 1;
-  bool dense = dense0, list = false;
+  bool list = false;
   uint32_t tot_list = 0;
   // list rounds: 8-bit words (colours from the planes), bounded degree, dirty marks available
   const bool can_list = sizeof(S) == 1 && PUSH && p.list_ok && p.dirty && head().maxdeg <= 64u;
@@ -1628,7 +1700,14 @@ __device__ __forceinline__ void sgr_body(const Params& p) {
       else if (dense) phase_a_dense<S, POL, CW>(p, r, mark, wk);
       else phase_a<S, POL, PUSH, CW>(p, r, bins, Win, mark, wk);
       work_stamp(p, 4 * r - 3, r);
-      if (!grid_sync(p)) return;
+      if (!grid_sync(p)) {
+        // where a stopped run can be resumed with wider words (8-bit overflow in this Phase A)
+        if (blk(p) == 0 && threadIdx.x == 0) {
+          p.info->resume_r = list ? 0u : r;
+          p.info->resume_mode = dense ? 1u : 0u;
+        }
+        return;
+      }
     }
     if (stamp && r <= p.trace_cap) p.phase_ns[4 * r - 2] = globaltimer();
     // round r+1 runs as a list round when round r-1's winners x 4 (successors + 1) <= n
@@ -1749,6 +1828,16 @@ __global__ void __launch_bounds__(BLOCK) k_phase_b(Params p, uint32_t r, WE* W, 
 __global__ void __launch_bounds__(BLOCK) k_epilogue(Params p, uint32_t r) {
   epilogue<uint32_t>(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) p.info->rounds = r;
+}
+
+// 8-bit -> 16-bit state words in place (gc_color's widening after ST_NEED16): top bit = committed,
+// the rest = colour, in both widths.
+__global__ void __launch_bounds__(BLOCK) k_widen8(const uint8_t* __restrict__ s8, uint16_t* __restrict__ s16,
+                                                  int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < count; i += (int64_t)gridDim.x * BLOCK) {
+    const uint32_t x = s8[i];
+    s16[i] = (uint16_t)(((x & SW<uint8_t>::COMMIT) ? SW<uint16_t>::COMMIT : 0u) | (x & SW<uint8_t>::CMASK));
+  }
 }
 
 // Grid-barrier cost probe (diagnostics only: gc__bench_grid_sync).

@@ -30,6 +30,13 @@ def test_design_bytes_per_unit_table():
     assert b.algorithmic_bytes(WORK, n) == expect
 
 
+def test_design_bytes_counts_issued_scatter_edges():
+    """Scatter edges skipped by the commit filter (neighbour seen committed) cost nothing."""
+    b = _bench()
+    n = 10
+    assert b.algorithmic_bytes(dict(WORK, scatter_reds=120), n) == b.algorithmic_bytes(WORK, n) - 8 * 80
+
+
 def test_survey_bytes_pull_model():
     """sum_{v in W_r} (24 + 8 deg) + sum (28 + 8 s_B), round 1 contributing m."""
     b = _bench()

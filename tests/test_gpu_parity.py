@@ -128,13 +128,23 @@ def test_bad_tuning_rejected(gc):
     assert e.value.status == 1
 
 
+@pytest.mark.parametrize("tuning", [{}, dict(widen=0), dict(dense_div=1000000000), dict(dense_div=0),
+                                    dict(n1=2, dense_div=1000000000)], ids=_tid)
 @pytest.mark.parametrize("k", [126, 127, 128, 129, 136])
-def test_state_word_restart(gc, k):
-    """8-bit state words hold colours <= 127: K_k needs colour k, so K_128 and beyond are
-    restarted with 16-bit words; colours up to 512 come from the 64 forbidden-colour planes,
-    beyond from the windowed fallback (reading C7)."""
-    res = _check(gc, wl.complete(k))
+def test_state_word_restart(gc, k, tuning):
+    """8-bit state words hold colours <= 127: K_k needs colour k, so from K_128 on the run stops
+    at the Phase A that overflows and goes on with 16-bit words — widened in place and resumed
+    there (default, in a dense or a sparse round), or restarted (widen=0); colours up to 512 come
+    from the 64 forbidden-colour planes, beyond from the windowed fallback (reading C7)."""
+    res = _check(gc, wl.complete(k), tuning=tuning)
     assert res.num_colors == k
+
+
+@pytest.mark.parametrize("tuning", [{}, dict(widen=0)], ids=_tid)
+def test_widen_graph500(gc, tuning):
+    """Graph500-skew R-MAT with > 127 colours: 8 -> 16-bit widening in place vs restart."""
+    res = _check(gc, wl.rmat(15, 32, wl.GRAPH500, 1), tuning=tuning)  # 136 colours, max degree 8673
+    assert res.num_colors > 127
 
 
 def test_multiwindow_colors(gc):
