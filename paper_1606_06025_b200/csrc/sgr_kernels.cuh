@@ -206,6 +206,9 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
 #ifndef GC_SYNC_SCATTER
 #define GC_SYNC_SCATTER 1
 #endif
+#ifndef GC_LOCAL_PASS1
+#define GC_LOCAL_PASS1 1
+#endif
 constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
 constexpr int WB = 32 * VPL;    // vertices per warp batch
 struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
@@ -727,8 +730,41 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 #endif
   constexpr bool RF = GC_RFILT && PUSH;
   if (RF) { cmw[2 * lane] = 0; cmw[2 * lane + 1] = 0; }
-  // conflict-scan passes
   uint32_t cap = PROBE;
+#if GC_LOCAL_PASS1
+  // pass 1, lane-local: the first PROBE positions of the lane's own scan range (nearest first),
+  // PROBE independent loads per lane and no owner search (the flattened passes below spend ~10
+  // shuffles per item finding owners and their segment data)
+  {
+    int32_t w[PROBE];
+#pragma unroll
+    for (int u = 0; u < PROBE; ++u) w[u] = state == 3 && (uint32_t)u < len ? ldc(p.ci, sbase + sdir * u) : -1;
+    int first = -1;
+    uint32_t cbits = 0;
+#pragma unroll
+    for (int u = PROBE - 1; u >= 0; --u) {
+      if (w[u] < 0) continue;
+      const uint32_t sv = ldnb(st + w[u]);
+      if (RF && (sv & SW<S>::COMMIT)) cbits |= 1u << u;
+      if ((sv & CM) == tent && recolors<POL>(p, e.v, w[u], dv)) first = u;
+    }
+    if (RF) cmw[2 * lane] = cbits;
+    if (state == 3) {
+      if (first >= 0) {
+        state = 1;
+        if (CW) { wk.v[W_B_EDGE] += first + 1; wk.v[W_B_GATHER] += first + 1; }
+      } else {
+        pos = len < (uint32_t)PROBE ? len : (uint32_t)PROBE;
+        if (pos == len) {
+          state = 2;
+          if (CW) { wk.v[W_B_EDGE] += len; wk.v[W_B_GATHER] += len; }
+        }
+      }
+    }
+    cap = 3 * PROBE;
+  }
+#endif
+  // conflict-scan passes
   for (;;) {
     const bool und = state == 3;
     if (!__any_sync(FULL, und)) break;
