@@ -209,6 +209,9 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
 #ifndef GC_LOCAL_PASS1
 #define GC_LOCAL_PASS1 1
 #endif
+#ifndef GC_LOCAL_SCATTER
+#define GC_LOCAL_SCATTER 8        // sparse batches: rows up to this length scattered lane-locally
+#endif
 constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
 constexpr int WB = 32 * VPL;    // vertices per warp batch
 struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
@@ -834,6 +837,35 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     if (sc && end < 0) end = RP(p, e.v + 1);
     const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
     if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter && !RF) wk.v[W_SCATTER_RED] += Wn; }
+#if GC_LOCAL_SCATTER
+    // short rows only (bounded-degree graphs): every lane scatters its own winner's row, up to
+    // GC_LOCAL_SCATTER entries 4 loads at a time, without the flattened loop's owner search
+    if (!p.sfilter && __reduce_max_sync(FULL, Wn) <= (uint32_t)GC_LOCAL_SCATTER) {
+      if (Wn) {
+        uint8_t* const pl = (dist(p) ? nullptr : p.fmp) + (int64_t)((tent - 1) >> 3) * p.plane;
+        const uint32_t bit = 1u << ((tent - 1) & 7);
+#pragma unroll
+        for (uint32_t j0 = 0; j0 < (uint32_t)GC_LOCAL_SCATTER; j0 += 4) {
+          if (j0 >= Wn) break;
+          int32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t j = j0 + u;
+            const bool skip = RF && j < Wn && rfilt_skip<POL>(cmw + 2 * lane, (int64_t)j, e.k);
+            w[u] = j < Wn && !skip ? ldc(p.ci, e.beg + j) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (w[u] >= 0) {
+              if (dist(p)) red_color<S>(p, (int64_t)((tent - 1) >> 3) * p.plane, w[u], bit);
+              else red_plane<S>(pl, w[u], bit);
+              if (CW && RF) wk.v[W_SCATTER_RED] += 1;
+            }
+        }
+      }
+      return state;
+    }
+#endif
     const uint32_t E = warp_incl_scan(Wn, lane);
     const uint32_t T = __shfl_sync(FULL, E, 31);
     if (GC_SYNC_SCATTER || RF) __syncwarp();  // the scans' committed masks (RF)
