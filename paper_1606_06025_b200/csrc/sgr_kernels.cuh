@@ -599,6 +599,17 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
           if (CW) wk.v[W_MARK] += (unsigned long long)(hi - lo + 1);
         }
         const uint32_t Wn = (uint32_t)(hi - lo);
+#if GC_LOCAL_SCATTER
+        if (__reduce_max_sync(FULL, Wn) <= 4u) {  // short successor ranges: every lane its own
+          int32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w[u] = (uint32_t)u < Wn ? ldc(p.ci, lo + u) : -1;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (w[u] >= 0) sts(dirty_of(p, w[u]) + w[u], 1u);
+          continue;
+        }
+#endif
         const uint32_t E = warp_incl_scan(Wn, lane);
         const uint32_t T = __shfl_sync(FULL, E, 31);
         for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
