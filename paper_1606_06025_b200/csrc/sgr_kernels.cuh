@@ -1283,6 +1283,29 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       Wh[h] = ((states >> (8 * h)) & 0xffu) == 2u && sg.tent[sl] <= 8u * p.np ? sg.deg[sl] : 0u;
       if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter && !GC_RFILT) wk.v[W_SCATTER_RED] += Wh[h]; }
     }
+#if GC_LOCAL_SCATTER
+    // short rows only: every lane scatters its own slots' rows (at most 4 entries each)
+    uint32_t wmax = 0;
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) wmax = Wh[h] > wmax ? Wh[h] : wmax;
+    if (!p.sfilter && !GC_RFILT && __reduce_max_sync(FULL, wmax) <= 4u) {
+      int32_t w[VPL][4];
+#pragma unroll
+      for (int h = 0; h < VPL; ++h) {
+        const int sl = lane * VPL + h;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[h][u] = (uint32_t)u < Wh[h] ? ldc(p.ci, seg_beg<POL>(sg, sl) + u) : -1;
+      }
+#pragma unroll
+      for (int h = 0; h < VPL; ++h) {
+        const uint32_t t = sg.tent[lane * VPL + h];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (w[h][u] >= 0) red_color<S>(p, (int64_t)((t - 1) >> 3) * p.plane, w[h][u], 1u << ((t - 1) & 7));
+      }
+    } else
+#endif
+    {
     const uint32_t T = seg_prefix(sg, Wh, lane);
     for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
       int32_t w[4];
@@ -1315,6 +1338,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
         red_color<S>(p, (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
         if (CW && (p.sfilter || GC_RFILT)) wk.v[W_SCATTER_RED] += 1;
       }
+    }
     }
     __syncwarp();
   }
