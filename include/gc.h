@@ -114,7 +114,7 @@ typedef struct gc_tuning {
   int32_t dense_div;       /* dense (id-order) rounds while |W_r| * dense_div > n; 0 = never dense;
                               default 3.  A non-negative value also sets dense_div_n1 unless that
                               is given explicitly */
-  int32_t dense_div_n1;    /* the same in dirty-set rounds; default 16 */
+  int32_t dense_div_n1;    /* the same in dirty-set rounds; default 32 */
   int32_t n1;              /* dirty-set rounds: 0 off, 1 when max degree <= 64 (default), 2 always */
   int32_t list;            /* explicit list rounds: 0 off (default), 1 cost rule, 2 from round 3 */
   int32_t compact;         /* dense Phase B lists pending vertices without marks: 0 (default) / 1 */

@@ -201,7 +201,7 @@ void launch_b(int pol, bool push, bool cw, int grid, cudaStream_t s, const Param
 // Schedule knobs (include/gc.h gc_tuning), resolved to the measured defaults.
 struct Knobs {
   int state_bytes = 1;  // first attempt's state-word width
-  uint32_t dense_div = 3, dense_div_n1 = 16, n1 = 1, list = 0, compact = 0, sfilter = 0, dch = 16, n1_chg = 0;
+  uint32_t dense_div = 3, dense_div_n1 = 32, n1 = 1, list = 0, compact = 0, sfilter = 0, dch = 16, n1_chg = 0;
   int variant = -1;
   uint32_t watchdog_ms = 0;  // 0 = 60 s
   uint32_t widen = 1;        // 8-bit overflow: widen in place and resume (1) or restart (0)
@@ -509,7 +509,7 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
   p.compact = kn.compact;
   p.dch = kn.dch;            // sweep 2..32 on the three configs: 16 (R-MAT s24 -1 %)
   p.n1chg = kn.n1_chg;
-  p.dense_div_n1 = kn.dense_div_n1;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16
+  p.dense_div_n1 = kn.dense_div_n1;  // sweep with dirty-set rounds (stencil, mesh): 4..256 -> 16 (round 1), 32 (round 2)
   p.ksplit = (int32_t*)ksplit;
   p.dirty = (uint8_t*)dirty;
   p.wlw0 = (int32_t*)wlw0;
