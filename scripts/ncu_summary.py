@@ -8,7 +8,8 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.sum.per_second",
+        "dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "lts__t_sectors.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size",
@@ -16,8 +17,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_read.sum",
         "lts__t_sectors_op_write.sum"]
 def find(w):
-    """Column of metric w: exact name, else a prefixed variant (this ncu reports e.g.
-    FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed), else the .ratio
+    """Column of metric w: exact name, else a prefixed variant, else the .ratio
     form of a .pct metric (smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio)."""
     cands = [w] + ([w[:-4] + ".ratio"] if w.endswith(".pct") else [])
     for c in cands:
