@@ -144,9 +144,8 @@ def algorithmic_bytes(work, n):
                sparse, per entry         : WE 16 + sw
                per examined position     : col 4 + sw
                per vertex (commit, once) : sw;  per pushed loser : WE 16
-               per scatter edge issued   : col 4 + RED 4 (scatter_reds: edges into neighbours
-                                           seen committed by the winner's own scan are skipped,
-                                           neither loaded nor REDed — GC_RFILT)
+               per scatter edge          : col 4 + RED 4 (counted as scatter_reds, which equals
+                                           commit_scatter unless gc_tuning.scatter_filter)
       finalize per vertex : sw + colour 4
     """
     sw = int(work.get("state_bytes") or 1)

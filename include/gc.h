@@ -86,10 +86,8 @@ typedef struct gc_work {
   uint64_t phase_b_gathers;    /* neighbour colour words gathered by the conflict scans */
   uint64_t commit_scatter;     /* neighbour entries visited by the commit scatters */
   uint64_t pushes;             /* vertices pushed into W_out over the run */
-  uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters (entries whose neighbour
-                                   the winner saw committed during its own scan are skipped; a
-                                   neighbour committing in the same phase may be seen either way,
-                                   so this one counter can vary between runs) */
+  uint64_t scatter_reds;       /* forbidden-mask atomics issued by the commit scatters (fewer than
+                                   commit_scatter only with gc_tuning.scatter_filter) */
   uint64_t dense_a_swept;      /* vertices swept by dense (id-order) Phase A passes */
   uint64_t dense_b_swept;      /* vertices swept by dense Phase B passes */
   uint64_t sparse_a_entries;   /* worklist entries read by sparse Phase A passes */

@@ -556,9 +556,6 @@ gc_status gc_color(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, co
       p.st = (uint8_t*)planes - (int64_t)sbytes * pitch;
       void* fn = pick_persistent(sbytes, (int)o.policy, push, cw, fat);
       int per_sm = 0;
-#ifdef GC_CARVEOUT
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, GC_CARVEOUT));
-#endif
       CK(occupancy(dev, fn, &per_sm));
       if (per_sm < 1) {
         set_err("gc_color: persistent kernel cannot be resident");

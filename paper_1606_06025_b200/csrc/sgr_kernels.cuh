@@ -197,15 +197,6 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
 #ifndef GC_VPL
 #define GC_VPL 2
 #endif
-#ifndef GC_RFILT
-#define GC_RFILT 0
-#endif
-#ifndef GC_CMSMEM
-#define GC_CMSMEM 1
-#endif
-#ifndef GC_SYNC_SCATTER
-#define GC_SYNC_SCATTER 1
-#endif
 #ifndef GC_LOCAL_PASS1
 #define GC_LOCAL_PASS1 1
 #endif
@@ -223,9 +214,6 @@ struct WideSeg {                // per-warp segment table of one dense batch (sl
   int first[WB];                // work counters: first hit
   uint32_t tent[WB];
   uint32_t lost[VPL];
-#if GC_CMSMEM
-  uint32_t cm[WB][2];           // scan positions 0..63 whose neighbour was seen committed (GC_RFILT)
-#endif
 };
 struct BSmem {
   WE pbuf[WARPS][PBUF];   // per-warp push staging (Pusher, bin 0)
@@ -236,9 +224,6 @@ struct BSmem {
   int first;              // conflict_cta
   int32_t k;              // cta_vertex split broadcast
   int cwfirst[WARPS][32]; // work counters: first hit per lane's vertex
-#if GC_CMSMEM
-  uint32_t cm[WARPS][64];  // sparse batches: per lane, scan positions 0..63 seen committed (GC_RFILT)
-#endif
 };
 __device__ __forceinline__ BSmem& bsmem() {
   __shared__ BSmem s;
@@ -698,19 +683,6 @@ __device__ __forceinline__ void rec_winners(const Params& p, uint32_t r, bool wi
   if (win) ((r & 1) ? p.wlw1 : p.wlw0)[pos + __popc(m & lanemask_lt())] = v;
 }
 
-// Commit-scatter filter (GC_RFILT): a winner has examined its whole scan range, so it knows which
-// of those neighbours were committed (before or during this phase).  A committed vertex never
-// reads its forbidden-colour planes again, so the RED into its plane byte is useless (about a
-// third of all REDs on R-MAT): the scans record "committed" for scan positions 0..63 in a
-// per-slot 64-bit mask in shared memory and the scatter skips those neighbours.  Row offset x of
-// the owner's row maps to scan position j (HIGHER_ID: k-1-x below the split; LOWER_ID: x-k above
-// it; DEGREE: x); positions outside [0, 64) are always scattered.
-template <int POL>
-__device__ __forceinline__ bool rfilt_skip(const uint32_t* cm2, int64_t x, int32_t k) {
-  const int64_t j = POL == HIGHER_ID ? (int64_t)k - 1 - x : (POL == LOWER_ID ? x - k : x);
-  return j >= 0 && j < 64 && ((cm2[j >> 5] >> (j & 31)) & 1u);
-}
-
 // One batch of up to 32 vertices, one per lane (act).  The conflict scans of all of them
 // advance together in passes over the flattened segments: pass 1 examines the first 4
 // positions of every scan range (the nearest lower ids, where most conflicts are), later
@@ -737,13 +709,6 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     if (POL == DEGREE) dv = end - e.beg;
     state = len ? 3 : 2;
   }
-#if GC_RFILT
-  uint32_t* const cmw = bsmem().cm[threadIdx.x >> 5];
-#else
-  uint32_t* const cmw = nullptr;
-#endif
-  constexpr bool RF = GC_RFILT && PUSH;
-  if (RF) { cmw[2 * lane] = 0; cmw[2 * lane + 1] = 0; }
   uint32_t cap = PROBE;
 #if GC_LOCAL_PASS1
   // pass 1, lane-local: the first PROBE positions of the lane's own scan range (nearest first),
@@ -754,15 +719,12 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 #pragma unroll
     for (int u = 0; u < PROBE; ++u) w[u] = state == 3 && (uint32_t)u < len ? ldc(p.ci, sbase + sdir * u) : -1;
     int first = -1;
-    uint32_t cbits = 0;
 #pragma unroll
     for (int u = PROBE - 1; u >= 0; --u) {
       if (w[u] < 0) continue;
       const uint32_t sv = ldnb(st + w[u]);
-      if (RF && (sv & SW<S>::COMMIT)) cbits |= 1u << u;
       if ((sv & CM) == tent && recolors<POL>(p, e.v, w[u], dv)) first = u;
     }
-    if (RF) cmw[2 * lane] = cbits;
     if (state == 3) {
       if (first >= 0) {
         state = 1;
@@ -813,7 +775,6 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         const int64_t dvo = POL == DEGREE ? __shfl_sync(FULL, dv, oc) : 0;
         const uint32_t sv = own[u] >= 0 ? ldnb(st + w[u]) : 0u;
         const bool hit = own[u] >= 0 && (sv & CM) == to && recolors<POL>(p, vo, w[u], dvo);
-        if (RF && (sv & SW<S>::COMMIT) && jj[u] < 64) atomicOr(&cmw[2 * oc + (int)(jj[u] >> 5)], 1u << (jj[u] & 31));
         if (hit) {
           lost |= 1u << oc;
           if (CW) atomicMin(&s_first[oc], (int)jj[u]);
@@ -847,7 +808,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
     const bool sc = win && tent <= 8u * p.np;
     if (sc && end < 0) end = RP(p, e.v + 1);
     const uint32_t Wn = sc ? (uint32_t)(end - e.beg) : 0u;
-    if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter && !RF) wk.v[W_SCATTER_RED] += Wn; }
+    if (CW) { wk.v[W_SCATTER] += Wn; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wn; }
 #if GC_LOCAL_SCATTER
     // short rows only (bounded-degree graphs): every lane scatters its own winner's row, up to
     // GC_LOCAL_SCATTER entries 4 loads at a time, without the flattened loop's owner search
@@ -862,15 +823,13 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t j = j0 + u;
-            const bool skip = RF && j < Wn && rfilt_skip<POL>(cmw + 2 * lane, (int64_t)j, e.k);
-            w[u] = j < Wn && !skip ? ldc(p.ci, e.beg + j) : -1;
+            w[u] = j < Wn ? ldc(p.ci, e.beg + j) : -1;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (w[u] >= 0) {
               if (dist(p)) red_color<S>(p, (int64_t)((tent - 1) >> 3) * p.plane, w[u], bit);
               else red_plane<S>(pl, w[u], bit);
-              if (CW && RF) wk.v[W_SCATTER_RED] += 1;
             }
         }
       }
@@ -879,7 +838,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
 #endif
     const uint32_t E = warp_incl_scan(Wn, lane);
     const uint32_t T = __shfl_sync(FULL, E, 31);
-    if (GC_SYNC_SCATTER || RF) __syncwarp();  // the scans' committed masks (RF)
+    __syncwarp();
     for (uint32_t f0 = 0; f0 < T; f0 += 32 * 4) {
       int32_t w[4];
       uint32_t wb[4];
@@ -892,10 +851,8 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
         const uint32_t Eo = __shfl_sync(FULL, E, oc), Wo = __shfl_sync(FULL, Wn, oc);
         const int64_t bo = __shfl_sync(FULL, e.beg, oc);
         const uint32_t to = __shfl_sync(FULL, tent, oc);
-        const int32_t ko = RF ? __shfl_sync(FULL, e.k, oc) : 0;
         wb[u] = 1u << ((to - 1) & 7);
-        const bool skip = RF && f < T && rfilt_skip<POL>(cmw + 2 * oc, (int64_t)(f - (Eo - Wo)), ko);
-        w[u] = f < T && !skip ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
+        w[u] = f < T ? ldc(p.ci, bo + (f - (Eo - Wo))) : -1;
         pl[u] = (dist(p) && w[u] >= 0 ? fmp_of(p, w[u]) : p.fmp) + (int64_t)((to - 1) >> 3) * p.plane;
       }
       if (p.sfilter) {
@@ -911,10 +868,7 @@ __device__ __forceinline__ int batch_b(const Params& p, int lane, bool act, cons
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (w[u] >= 0) {
-            red_plane<S>(pl[u], w[u], wb[u]);
-            if (CW && RF) wk.v[W_SCATTER_RED] += 1;
-          }
+          if (w[u] >= 0) red_plane<S>(pl[u], w[u], wb[u]);
       }
     }
   }
@@ -1170,17 +1124,12 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
       if (((states >> (8 * h)) & 0xffu) != 3u) continue;
       const uint32_t t = sg.tent[sl];
       int first = -1;
-      uint32_t cbits = 0;
 #pragma unroll
       for (int u = PROBE - 1; u >= 0; --u) {
         const uint32_t sv = w[h][u] >= 0 ? ldnb(st + w[h][u]) : 0u;
-        if (GC_RFILT && PUSH && (sv & SW<S>::COMMIT)) cbits |= 1u << u;
         if (w[h][u] >= 0 && (sv & CM) == t && recolors<POL>(p, (int32_t)(base + sl), w[h][u], (int64_t)sg.deg[sl]))
           first = u;
       }
-#if GC_RFILT
-      if (PUSH) { sg.cm[sl][0] = cbits; sg.cm[sl][1] = 0; }
-#endif
       const uint32_t len = seg_len<POL>(sg, sl);
       if (first >= 0) {
         states ^= 2u << (8 * h);  // 3 -> 1
@@ -1233,9 +1182,6 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
           const int o = own[u];
           const uint32_t sv = ldnb(st + w[u]);
           const bool hit = (sv & CM) == sg.tent[o] && recolors<POL>(p, (int32_t)(base + o), w[u], (int64_t)sg.deg[o]);
-#if GC_RFILT
-          if (PUSH && (sv & SW<S>::COMMIT) && jj[u] < 64) atomicOr(&sg.cm[o][jj[u] >> 5], 1u << (jj[u] & 31));
-#endif
           if (hit) {
             atomicOr(&sg.lost[o >> 5], 1u << (o & 31));
             if (CW) atomicMin(&sg.first[o], (int)jj[u]);
@@ -1281,14 +1227,14 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
     for (int h = 0; h < VPL; ++h) {
       const int sl = lane * VPL + h;
       Wh[h] = ((states >> (8 * h)) & 0xffu) == 2u && sg.tent[sl] <= 8u * p.np ? sg.deg[sl] : 0u;
-      if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter && !GC_RFILT) wk.v[W_SCATTER_RED] += Wh[h]; }
+      if (CW) { wk.v[W_SCATTER] += Wh[h]; if (!p.sfilter) wk.v[W_SCATTER_RED] += Wh[h]; }
     }
 #if GC_LOCAL_SCATTER
     // short rows only: every lane scatters its own slots' rows (at most 4 entries each)
     uint32_t wmax = 0;
 #pragma unroll
     for (int h = 0; h < VPL; ++h) wmax = Wh[h] > wmax ? Wh[h] : wmax;
-    if (!p.sfilter && !GC_RFILT && __reduce_max_sync(FULL, wmax) <= 4u) {
+    if (!p.sfilter && __reduce_max_sync(FULL, wmax) <= 4u) {
       int32_t w[VPL][4];
 #pragma unroll
       for (int h = 0; h < VPL; ++h) {
@@ -1319,9 +1265,6 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
           const int o = seg_owner(sg.E, f);
           own[u] = o;
           const uint32_t x = f - (o ? sg.E[o - 1] : 0u);
-#if GC_RFILT
-          if (rfilt_skip<POL>(sg.cm[o], (int64_t)x, sg.k[o])) continue;
-#endif
           w[u] = ldc(p.ci, seg_beg<POL>(sg, o) + x);
         }
       }
@@ -1336,7 +1279,7 @@ __device__ __forceinline__ void batch_b_wide(const Params& p, int lane, uint32_t
         if (w[u] < 0 || (skip >> u & 1u)) continue;
         const uint32_t t = sg.tent[own[u]];
         red_color<S>(p, (int64_t)((t - 1) >> 3) * p.plane, w[u], 1u << ((t - 1) & 7));
-        if (CW && (p.sfilter || GC_RFILT)) wk.v[W_SCATTER_RED] += 1;
+        if (CW && p.sfilter) wk.v[W_SCATTER_RED] += 1;
       }
     }
     }
