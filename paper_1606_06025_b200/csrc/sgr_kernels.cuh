@@ -203,6 +203,9 @@ __device__ __forceinline__ int flat_owner(uint32_t E, uint32_t f) {
 #ifndef GC_LOCAL_SCATTER
 #define GC_LOCAL_SCATTER 8        // sparse batches: rows up to this length scattered lane-locally
 #endif
+#ifndef GC_LOCAL_MARK
+#define GC_LOCAL_MARK 16          // dense Phase A: successor ranges up to this length marked lane-locally
+#endif
 constexpr int VPL = GC_VPL;     // dense batches: consecutive vertices per lane
 constexpr int WB = 32 * VPL;    // vertices per warp batch
 struct WideSeg {                // per-warp segment table of one dense batch (slot = vertex - base)
@@ -585,13 +588,17 @@ __device__ __forceinline__ void phase_a_dense(const Params& p, uint32_t r, bool 
         }
         const uint32_t Wn = (uint32_t)(hi - lo);
 #if GC_LOCAL_SCATTER
-        if (__reduce_max_sync(FULL, Wn) <= 4u) {  // short successor ranges: every lane its own
-          int32_t w[4];
+        if (__reduce_max_sync(FULL, Wn) <= (uint32_t)GC_LOCAL_MARK) {  // short ranges: every lane its own
 #pragma unroll
-          for (int u = 0; u < 4; ++u) w[u] = (uint32_t)u < Wn ? ldc(p.ci, lo + u) : -1;
+          for (uint32_t j0 = 0; j0 < (uint32_t)GC_LOCAL_MARK; j0 += 4) {
+            if (j0 >= Wn) break;
+            int32_t w[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (w[u] >= 0) sts(dirty_of(p, w[u]) + w[u], 1u);
+            for (int u = 0; u < 4; ++u) w[u] = j0 + u < Wn ? ldc(p.ci, lo + j0 + u) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (w[u] >= 0) sts(dirty_of(p, w[u]) + w[u], 1u);
+          }
           continue;
         }
 #endif
